@@ -4,30 +4,36 @@
 NVCC ?= /usr/local/cuda/bin/nvcc
 CC ?= gcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-# No fast-math, no FMA contraction, IEEE division/sqrt, no flush-to-zero: the codes must be
+# No fast-math, no FMA contraction, IEEE division, no flush-to-zero: the codes must be
 # bit-identical to the oracle.
-NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xptxas -v --fmad=false -ftz=false \
-           -prec-div=true -prec-sqrt=true -Xcompiler -fPIC,-ffp-contract=off,-O2 \
-           -Iinclude -shared -cudart static
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo --fmad=false -ftz=false -prec-div=true \
+           -prec-sqrt=true -Xcompiler -fPIC,-ffp-contract=off -Iinclude
 ORACLE_CFLAGS := -O2 -std=gnu11 -fPIC -shared -ffp-contract=off -frounding-math \
                  -fno-fast-math -Wall -Wextra
 
 PKG := paper_2206_11357_b200
-LIB_SRCS := $(PKG)/csrc/gact_kernels.cu $(PKG)/csrc/gact_host.cu
-LIB_HDRS := include/gact.h $(wildcard $(PKG)/csrc/*.cuh)
+CSRC := $(PKG)/csrc
+OBJDIR := build/obj
+LIB_SRCS := $(wildcard $(CSRC)/*.cu)
+LIB_OBJS := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(LIB_SRCS))
+LIB_HDRS := include/gact.h $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h)
 
 all: lib oracle
 
 lib: $(PKG)/libgact.so
 oracle: oracle/liboracle.so
 
-$(PKG)/libgact.so: $(LIB_SRCS) $(LIB_HDRS)
-	$(NVCC) $(NVFLAGS) -o $@ $(LIB_SRCS) 2> $(PKG)/ptxas.log || (cat $(PKG)/ptxas.log; exit 1)
+$(OBJDIR)/%.o: $(CSRC)/%.cu $(LIB_HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c -o $@ $< 2> $(OBJDIR)/$*.ptxas.log || (cat $(OBJDIR)/$*.ptxas.log; exit 1)
+
+$(PKG)/libgact.so: $(LIB_OBJS)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(LIB_OBJS)
 
 oracle/liboracle.so: oracle/gact_oracle.c oracle/gact_oracle.h
 	$(CC) $(ORACLE_CFLAGS) -o $@ oracle/gact_oracle.c -lm
 
 clean:
-	rm -f $(PKG)/libgact.so oracle/liboracle.so $(PKG)/ptxas.log
+	rm -rf build $(PKG)/libgact.so oracle/liboracle.so
 
 .PHONY: all lib oracle clean

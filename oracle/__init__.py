@@ -221,3 +221,20 @@ def allocate_bruteforce(c, D, ladder, B: int):
     rc = lib().oracle_allocate_bruteforce(_ptr(c), _ptr(D), c.size, _ptr(lad), lad.size, B,
                                           _ptr(out), _ptr(val))
     return rc, out[:c.size], float(val[0])
+
+
+def quantize_codes_span(x_span: np.ndarray, tag: int, n: int, G: int, bits: int, seed: int,
+                        g0: int, g1: int):
+    """Like quantize_codes for groups [g0, g1) of an n-element tensor, given only the host
+    copy of those groups' elements (x_span = x[g0*G : min(g1*G, n)]). The oracle indexes the
+    tensor by global element index; the base pointer is offset so that only the span is read."""
+    x_span = np.ascontiguousarray(x_span).reshape(-1)
+    count = min(g1 * G, n) - g0 * G
+    assert x_span.size == count and g1 > g0
+    base = x_span.ctypes.data - g0 * G * x_span.itemsize
+    q = np.zeros(count, dtype=np.uint8)
+    mn = np.zeros(g1 - g0, dtype=np.float32)
+    sc = np.zeros_like(mn)
+    _check(lib().oracle_quantize_codes(base, tag, n, G, bits, seed, g0, g1, _ptr(q), _ptr(mn),
+                                       _ptr(sc)), "quantize_codes_span")
+    return q, mn, sc

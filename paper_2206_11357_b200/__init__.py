@@ -1,0 +1,236 @@
+"""paper_2206_11357_b200 — B200-native GACT activation-compressor hot path.
+
+Thin Python binding of the C ABI in include/gact.h (libgact.so, sm_100a CUDA kernels):
+argument marshalling only. PyTorch supplies device memory (the caching allocator),
+streams (the current stream is passed to every call) and process groups (dist.py).
+Every step of the path runs in libgact's kernels; there is no CPU fallback: functions
+raise if the library is missing or a tensor is not on a CUDA device.
+
+Names follow the paper (arXiv 2206.11357): bits b, group size G, per-group min and scale,
+sensitivity c_l, numel D_l, budget B (P:n = /root/reference/PAPER.md line n):
+  quantize_pack        Q_b(h^(l))    App. Prop. 3
+  unpack_dequantize    T^{-1}
+  group_stats          min/max
+  allocate_bits        eqn:ilp       P:471-475, greedy P:534
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Sequence
+
+import numpy as np
+import torch
+
+__all__ = [
+    "lib", "GactError", "F32", "BF16", "F16", "DEFAULT_GROUP", "LADDER",
+    "num_groups", "packed_words", "group_stats", "quantize_pack", "unpack_dequantize",
+    "quantize_pack_batch", "unpack_dequantize_batch", "allocate_bits", "CompressedTensor",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgact.so")
+
+F32, BF16, F16 = 0, 1, 2
+DEFAULT_GROUP = 256
+LADDER = (1, 2, 4, 8)
+MAX_BATCH = 256
+_TORCH_TAG = {torch.float32: F32, torch.bfloat16: BF16, torch.float16: F16}
+_TAG_TORCH = {v: k for k, v in _TORCH_TAG.items()}
+
+
+class GactError(RuntimeError):
+    """A libgact call returned a non-OK gact_status."""
+
+    def __init__(self, fn: str, status: int):
+        self.status = status
+        name = lib().gact_status_string(status).decode()
+        super().__init__(f"{fn}: {name} ({status})")
+
+
+class _Desc(ctypes.Structure):
+    """gact_tensor_desc (include/gact.h)."""
+    _fields_ = [
+        ("data", ctypes.c_void_p), ("packed", ctypes.c_void_p),
+        ("group_min", ctypes.c_void_p), ("group_scale", ctypes.c_void_p),
+        ("n", ctypes.c_int64), ("seed", ctypes.c_uint64),
+        ("bits", ctypes.c_int32), ("dtype", ctypes.c_int32),
+    ]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded libgact.so (raises if it has not been built: no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with `make lib` "
+                              "(or __graft_entry__.build()); there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        P, i32, i64, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
+        sig = {
+            "gact_version": (i32, []),
+            "gact_status_string": (ctypes.c_char_p, [i32]),
+            "gact_num_groups": (i64, [i64, i32]),
+            "gact_packed_words": (i64, [i64, i32]),
+            "gact_group_stats": (i32, [P, i32, i64, i32, i32, P, P, P]),
+            "gact_quantize_pack": (i32, [P, i32, i64, i32, i32, u64, P, P, P, P]),
+            "gact_unpack_dequantize": (i32, [P, P, P, i64, i32, i32, P, i32, P]),
+            "gact_quantize_pack_batch": (i32, [ctypes.POINTER(_Desc), i32, i32, P]),
+            "gact_unpack_dequantize_batch": (i32, [ctypes.POINTER(_Desc), i32, i32, P]),
+            "gact_allocate_bits": (i32, [P, P, i32, P, i32, u64, P]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(fn: str, status: int) -> None:
+    if status != 0:
+        raise GactError(fn, status)
+
+
+def _stream(t: torch.Tensor) -> int:
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _require_cuda(*ts: torch.Tensor) -> None:
+    for t in ts:
+        if not t.is_cuda:
+            raise ValueError("libgact runs on CUDA tensors only (no CPU fallback)")
+
+
+def num_groups(n: int, group_size: int = DEFAULT_GROUP) -> int:
+    return int(lib().gact_num_groups(n, group_size))
+
+
+def packed_words(n: int, bits: int) -> int:
+    return int(lib().gact_packed_words(n, bits))
+
+
+class CompressedTensor:
+    """Q_b(h^(l)): packed codes + per-group (min, scale), and how to undo it."""
+    __slots__ = ("packed", "group_min", "group_scale", "shape", "dtype", "bits", "group_size", "seed")
+
+    def __init__(self, packed, group_min, group_scale, shape, dtype, bits, group_size, seed):
+        self.packed, self.group_min, self.group_scale = packed, group_min, group_scale
+        self.shape, self.dtype, self.bits, self.group_size, self.seed = shape, dtype, bits, group_size, seed
+
+    @property
+    def numel(self) -> int:
+        return int(np.prod(self.shape)) if len(self.shape) else 1
+
+    def nbytes(self) -> int:
+        return (self.packed.numel() * 4 + self.group_min.numel() * 4 + self.group_scale.numel() * 4)
+
+    def decompress(self, out: torch.Tensor | None = None) -> torch.Tensor:
+        return unpack_dequantize(self.packed, self.group_min, self.group_scale, self.numel,
+                                 self.bits, self.group_size, self.dtype, out=out).view(self.shape)
+
+
+def group_stats(x: torch.Tensor, bits: int, group_size: int = DEFAULT_GROUP):
+    """Per-group (min, scale) of a CUDA tensor (flattened row-major)."""
+    _require_cuda(x)
+    x = x.contiguous()
+    n = x.numel()
+    ng = max(num_groups(n, group_size), 0)
+    mn = torch.empty(ng, dtype=torch.float32, device=x.device)
+    sc = torch.empty(ng, dtype=torch.float32, device=x.device)
+    _check("gact_group_stats", lib().gact_group_stats(
+        x.data_ptr(), _TORCH_TAG[x.dtype], n, group_size, bits, mn.data_ptr(), sc.data_ptr(), _stream(x)))
+    return mn, sc
+
+
+def quantize_pack(x: torch.Tensor, bits: int, seed: int, group_size: int = DEFAULT_GROUP,
+                  out: tuple | None = None) -> CompressedTensor:
+    """Compress one context tensor: fused group min/max + stochastic rounding + packing."""
+    _require_cuda(x)
+    xc = x.contiguous()
+    n = xc.numel()
+    if out is None:
+        packed = torch.empty(max(packed_words(n, bits), 0), dtype=torch.int32, device=x.device)
+        mn = torch.empty(max(num_groups(n, group_size), 0), dtype=torch.float32, device=x.device)
+        sc = torch.empty_like(mn)
+    else:
+        packed, mn, sc = out
+    _check("gact_quantize_pack", lib().gact_quantize_pack(
+        xc.data_ptr(), _TORCH_TAG[x.dtype], n, group_size, bits, seed & (2**64 - 1),
+        packed.data_ptr(), mn.data_ptr(), sc.data_ptr(), _stream(xc)))
+    return CompressedTensor(packed, mn, sc, tuple(x.shape), x.dtype, bits, group_size, seed)
+
+
+def unpack_dequantize(packed: torch.Tensor, group_min: torch.Tensor, group_scale: torch.Tensor,
+                      n: int, bits: int, group_size: int = DEFAULT_GROUP,
+                      dtype: torch.dtype = torch.float32, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Decompress: y = RNE_dtype(fma(q, scale, mn)) for n elements."""
+    _require_cuda(packed, group_min, group_scale)
+    y = torch.empty(n, dtype=dtype, device=packed.device) if out is None else out
+    _check("gact_unpack_dequantize", lib().gact_unpack_dequantize(
+        packed.data_ptr(), group_min.data_ptr(), group_scale.data_ptr(), n, group_size, bits,
+        y.data_ptr(), _TORCH_TAG[y.dtype], _stream(packed)))
+    return y
+
+
+def _desc_array(rows) -> ctypes.Array:
+    arr = (_Desc * max(len(rows), 1))()
+    for i, r in enumerate(rows):
+        arr[i] = _Desc(*r)
+    return arr
+
+
+def quantize_pack_batch(xs: Sequence[torch.Tensor], bits: Sequence[int], seeds: Sequence[int],
+                        group_size: int = DEFAULT_GROUP, outs: Sequence[tuple] | None = None):
+    """Compress a whole context h = (h^(l)) with per-tensor bits in one launch per
+    (dtype, bits) class. Returns a list of CompressedTensor."""
+    res, rows = [], []
+    for i, (x, b, s) in enumerate(zip(xs, bits, seeds)):
+        _require_cuda(x)
+        if not x.is_contiguous():
+            raise ValueError("quantize_pack_batch needs contiguous tensors")
+        n = x.numel()
+        if outs is None:
+            packed = torch.empty(max(packed_words(n, b), 0), dtype=torch.int32, device=x.device)
+            mn = torch.empty(max(num_groups(n, group_size), 0), dtype=torch.float32, device=x.device)
+            sc = torch.empty_like(mn)
+        else:
+            packed, mn, sc = outs[i]
+        rows.append((x.data_ptr(), packed.data_ptr(), mn.data_ptr(), sc.data_ptr(), n,
+                     s & (2**64 - 1), b, _TORCH_TAG[x.dtype]))
+        res.append(CompressedTensor(packed, mn, sc, tuple(x.shape), x.dtype, b, group_size, s))
+    if rows:
+        _check("gact_quantize_pack_batch", lib().gact_quantize_pack_batch(
+            _desc_array(rows), len(rows), group_size, _stream(xs[0])))
+    return res
+
+
+def unpack_dequantize_batch(cts: Sequence[CompressedTensor], outs: Sequence[torch.Tensor] | None = None):
+    """Decompress a list of CompressedTensor (one launch per (dtype, bits) class)."""
+    ys, rows = [], []
+    gs = {c.group_size for c in cts}
+    if len(gs) > 1:
+        raise ValueError("one group size per batch")
+    for i, c in enumerate(cts):
+        y = torch.empty(c.shape, dtype=c.dtype, device=c.packed.device) if outs is None else outs[i]
+        rows.append((y.data_ptr(), c.packed.data_ptr(), c.group_min.data_ptr(),
+                     c.group_scale.data_ptr(), c.numel, 0, c.bits, _TORCH_TAG[y.dtype]))
+        ys.append(y)
+    if rows:
+        _check("gact_unpack_dequantize_batch", lib().gact_unpack_dequantize_batch(
+            _desc_array(rows), len(rows), gs.pop(), _stream(cts[0].packed)))
+    return ys
+
+
+def allocate_bits(sensitivity, numel, budget_bits: int, ladder: Sequence[int] = LADDER) -> np.ndarray:
+    """Greedy solution of eqn:ilp (host computation inside libgact)."""
+    c = np.ascontiguousarray(sensitivity, dtype=np.float64)
+    D = np.ascontiguousarray(numel, dtype=np.int64)
+    lad = np.ascontiguousarray(ladder, dtype=np.int32)
+    out = np.zeros(max(c.size, 1), dtype=np.int32)
+    _check("gact_allocate_bits", lib().gact_allocate_bits(
+        c.ctypes.data, D.ctypes.data, c.size, lad.ctypes.data, lad.size, int(budget_bits), out.ctypes.data))
+    return out[:c.size]

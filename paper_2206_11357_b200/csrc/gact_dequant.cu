@@ -1,0 +1,202 @@
+// gact_dequant.cu — fused unpack + dequantize kernels (steps a4-a5 of DESIGN.md §1;
+// T^{-1}_{h,b} of App. Prop. 3; "Decompressor dequantizes context tensors",
+// §5.2), sm_100a.
+//
+// A warp owns a 256-element tile at a time; each lane decodes a chunk of 8 elements:
+// one 1/2/4/8-byte load of its packed unit, one broadcast load of (mn, scale) of its group,
+// then per element  q = field(unit) ; qf = float(q) via the 2^23 magic number (FADD2) ;
+// y = fma(qf, scale, mn) (FFMA2, one rounding) ; RNE to the output dtype (F2FP pack) ;
+// one 16- or 32-byte store. U tiles are decoded per iteration for memory-level parallelism.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "gact_device.cuh"
+#include "gact_internal.h"
+
+namespace gact {
+
+namespace {
+
+template <int MAXB>
+__device__ __forceinline__ int advance_cursor(const DBatch<MAXB>& P, int cur, int64_t tile) {
+  if constexpr (MAXB > 1) {
+    while (cur + 1 < P.count && tile >= P.tile_start[cur + 1]) ++cur;
+  }
+  return cur;
+}
+
+// The chunk's unit; for b < 8 it lies inside one word (index < nwords since e0 < n), for
+// b = 8 its second word exists only if e0 + 4 < n.
+template <int BITS>
+__device__ __forceinline__ uint2 load_unit(const uint32_t* packed, int64_t e0, int64_t n) {
+  const unsigned char* bytes = reinterpret_cast<const unsigned char*>(packed) + (e0 * BITS) / 8;
+  if constexpr (BITS == 1) {
+    return make_uint2(__ldg(reinterpret_cast<const uint8_t*>(bytes)), 0u);
+  } else if constexpr (BITS == 2) {
+    return make_uint2(__ldg(reinterpret_cast<const uint16_t*>(bytes)), 0u);
+  } else if constexpr (BITS == 4) {
+    return make_uint2(__ldg(reinterpret_cast<const uint32_t*>(bytes)), 0u);
+  } else {
+    if (e0 + kChunk <= n) return __ldg(reinterpret_cast<const uint2*>(bytes));
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(bytes);
+    return make_uint2(__ldg(w), e0 + 4 < n ? __ldg(w + 1) : 0u);
+  }
+}
+
+// Bit pattern 0x4B00_0000 | q_j (the float 2^23 + q_j) of element j of the unit.
+template <int BITS>
+__device__ __forceinline__ uint32_t magic_code(uint2 u, int j) {
+  if constexpr (BITS == 8) {
+    const uint32_t w = j < 4 ? u.x : u.y;
+    // bytes: [q, 0x00, 0x00, 0x4B]
+    return __byte_perm(w, 0x4B000000u, 0x7540 | (j & 3));
+  } else {
+    return ((u.x >> (j * BITS)) & ((1u << BITS) - 1u)) | 0x4B000000u;
+  }
+}
+
+// y_j = fma(q_j, scale, mn) for the 8 elements of a unit, as 4 packed pairs.
+template <int BITS>
+__device__ __forceinline__ void decode8(uint2 u, float mn, float scale, float y[8]) {
+  const f2_t mn2 = f2_make(mn, mn), sc2 = f2_make(scale, scale);
+  const f2_t magic = f2_make(8388608.0f, 8388608.0f);
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const f2_t w2 = f2_bits(magic_code<BITS>(u, 2 * p), magic_code<BITS>(u, 2 * p + 1));
+    const f2_t q2 = f2_sub_rn(w2, magic);  // exact: q_j as float
+    f2_split(f2_fma_rn(q2, sc2, mn2), y[2 * p], y[2 * p + 1]);
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ void store8(void* ybase, int64_t e0, const float y[8]) {
+  if constexpr (DT == DT_F32) {
+    float4* p = reinterpret_cast<float4*>(static_cast<float*>(ybase) + e0);
+    __stcs(p, make_float4(y[0], y[1], y[2], y[3]));
+    __stcs(p + 1, make_float4(y[4], y[5], y[6], y[7]));
+  } else {
+    uint32_t w[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      if constexpr (DT == DT_BF16) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(y[2 * p], y[2 * p + 1]);
+        w[p] = *reinterpret_cast<uint32_t*>(&h);
+      } else {
+        __half2 h = __floats2half2_rn(y[2 * p], y[2 * p + 1]);
+        w[p] = *reinterpret_cast<uint32_t*>(&h);
+      }
+    }
+    uint4* p = reinterpret_cast<uint4*>(static_cast<uint16_t*>(ybase) + e0);
+    __stcs(p, make_uint4(w[0], w[1], w[2], w[3]));
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ void store1(void* ybase, int64_t e, float y) {
+  if constexpr (DT == DT_F32) {
+    static_cast<float*>(ybase)[e] = y;
+  } else if constexpr (DT == DT_BF16) {
+    static_cast<__nv_bfloat16*>(ybase)[e] = __float2bfloat16_rn(y);
+  } else {
+    static_cast<__half*>(ybase)[e] = __float2half_rn(y);
+  }
+}
+
+template <int DT, int BITS, int MAXB>
+__global__ void __launch_bounds__(kThreads)
+    dequantize_kernel(const __grid_constant__ DBatch<MAXB> P) {
+  constexpr int U = 4;
+  const int lane = threadIdx.x & 31;
+  const int64_t W = (int64_t)gridDim.x * kWarps;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  int cur = 0;
+  for (int64_t base = gw; base < P.tiles_total; base += (int64_t)U * W) {
+    int tix[U];
+    int64_t e[U];
+    bool valid[U];
+    uint2 unit[U];
+    float mn[U], sc[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t tile = base + (int64_t)k * W;
+      valid[k] = tile < P.tiles_total;
+      tix[k] = cur;
+      e[k] = 0;
+      if (valid[k]) {
+        cur = advance_cursor(P, cur, tile);
+        tix[k] = cur;
+        const DTensor& T = P.t[cur];
+        e[k] = (tile - P.tile_start[cur]) * kDequantTileElems + lane * kChunk;
+        valid[k] = e[k] < T.n;  // lanes past the end of a partial tile idle
+        if (valid[k]) {
+          unit[k] = load_unit<BITS>(T.packed, e[k], T.n);
+          const int64_t g = e[k] >> P.log2g;
+          mn[k] = __ldg(T.group_min + g);
+          sc[k] = __ldg(T.group_scale + g);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      if (!valid[k]) continue;
+      const DTensor& T = P.t[tix[k]];
+      float y[8];
+      decode8<BITS>(unit[k], mn[k], sc[k], y);
+      if (e[k] + kChunk <= T.n) {
+        store8<DT>(T.y, e[k], y);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (e[k] + j < T.n) store1<DT>(T.y, e[k] + j, y[j]);
+      }
+    }
+  }
+}
+
+template <typename K>
+int max_blocks_per_sm(K kernel) {
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, 0) != cudaSuccess || b < 1) b = 1;
+  return b;
+}
+
+template <int DT, int BITS, int MAXB>
+cudaError_t launch_d(const DBatch<MAXB>& p, cudaStream_t s) {
+  constexpr auto kernel = dequantize_kernel<DT, BITS, MAXB>;
+  static const int per_sm = max_blocks_per_sm(kernel);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (p.tiles_total + kWarps * 4 - 1) / (kWarps * 4);
+  const int64_t cap = (int64_t)sms * per_sm;
+  const int grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
+  kernel<<<grid, kThreads, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <int DT, int MAXB>
+cudaError_t launch_d_bits(const DBatch<MAXB>& p, int bits, cudaStream_t s) {
+  switch (bits) {
+    case 1: return launch_d<DT, 1, MAXB>(p, s);
+    case 2: return launch_d<DT, 2, MAXB>(p, s);
+    case 4: return launch_d<DT, 4, MAXB>(p, s);
+    default: return launch_d<DT, 8, MAXB>(p, s);
+  }
+}
+
+}  // namespace
+
+template <int MAXB>
+cudaError_t launch_dequantize(const DBatch<MAXB>& p, int dtype, int bits, cudaStream_t s) {
+  if (p.tiles_total == 0) return cudaSuccess;
+  switch (dtype) {
+    case DT_F32: return launch_d_bits<DT_F32, MAXB>(p, bits, s);
+    case DT_BF16: return launch_d_bits<DT_BF16, MAXB>(p, bits, s);
+    default: return launch_d_bits<DT_F16, MAXB>(p, bits, s);
+  }
+}
+
+template cudaError_t launch_dequantize<1>(const DBatch<1>&, int, int, cudaStream_t);
+template cudaError_t launch_dequantize<kMaxBatch>(const DBatch<kMaxBatch>&, int, int, cudaStream_t);
+
+}  // namespace gact

@@ -1,0 +1,292 @@
+// gact_device.cuh — device building blocks of the GACT compressor kernels (sm_100a).
+//
+// Product code. Implements the quantizer defined in include/gact.h (App. Prop. 3 of the
+// paper) with IEEE binary32 operations issued explicitly (no contraction):
+// the oracle/ directory is an independent CPU implementation used only by the tests.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gact {
+
+constexpr int kChunk = 8;       // elements per lane per Philox4x32-10 call (16-bit lanes)
+constexpr int kWarpTile = 256;  // 32 lanes x 8 elements: one coalesced warp pass
+constexpr int kWarps = 8;       // warps per CTA
+constexpr int kThreads = kWarps * 32;
+
+enum : int { DT_F32 = 0, DT_BF16 = 1, DT_F16 = 2 };
+
+// ------------------------------------------------------------------------ Philox4x32-10
+// Salmon et al., SC'11 (Random123 constants). key = seed, counter = (block lo, hi, 0, 0).
+__device__ __forceinline__ uint4 philox4x32_10(uint64_t block, uint32_t k0, uint32_t k1) {
+  uint32_t c0 = (uint32_t)block, c1 = (uint32_t)(block >> 32), c2 = 0u, c3 = 0u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
+    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+    c1 = (uint32_t)p1;
+    c3 = (uint32_t)p0;
+    c0 = n0;
+    c2 = n2;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return make_uint4(c0, c1, c2, c3);
+}
+
+// ------------------------------------------------------------------- packed f32x2 math
+// sm_100a executes these as FADD2 / FMUL2 / FFMA2 (two lanes of fp32 per instruction),
+// each lane correctly rounded in the stated mode — identical to two scalar IEEE ops.
+typedef unsigned long long f2_t;
+
+__device__ __forceinline__ f2_t f2_make(float lo, float hi) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_split(f2_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2_t f2_bits(uint32_t lo, uint32_t hi) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_split_bits(f2_t v, uint32_t& lo, uint32_t& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2_t f2_sub_rn(f2_t a, f2_t b) {
+  f2_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t f2_mul_rn(f2_t a, f2_t b) {
+  f2_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t f2_add_rm(f2_t a, f2_t b) {
+  f2_t r;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t f2_fma_rn(f2_t a, f2_t b, f2_t c) {
+  f2_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+__device__ __forceinline__ float min3f(float a, float b, float c) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+// Warp-wide fp32 min / max in one instruction (CREDUX on sm_100a).
+__device__ __forceinline__ float warp_min(float v) {
+  float r;
+  asm volatile("redux.sync.min.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ float warp_max(float v) {
+  float r;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+
+// ------------------------------------------------------------------- global memory I/O
+// Inputs are streamed once: read-only path, no L1 allocation.
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// 8 raw elements of one lane chunk: 32 bytes (f32) or 16 bytes (bf16 / f16).
+template <int DT>
+struct Raw8 {
+  uint4 a, b;
+};
+template <>
+struct Raw8<DT_BF16> {
+  uint4 a;
+};
+template <>
+struct Raw8<DT_F16> {
+  uint4 a;
+};
+
+template <int DT>
+__device__ __forceinline__ void load8(Raw8<DT>& r, const void* base, int64_t e) {
+  if constexpr (DT == DT_F32) {
+    const float* p = static_cast<const float*>(base) + e;
+    r.a = ldg_stream(p);
+    r.b = ldg_stream(p + 4);
+  } else {
+    const uint16_t* p = static_cast<const uint16_t*>(base) + e;
+    r.a = ldg_stream(p);
+  }
+}
+
+__device__ __forceinline__ float f16_bits_to_f32(uint32_t h) {
+  float f;
+  asm("{ .reg .f16 t; mov.b16 t, %1; cvt.f32.f16 %0, t; }" : "=f"(f) : "h"((unsigned short)h));
+  return f;
+}
+
+// Widen to binary32 (exact for every dtype). Element j of the chunk -> v[j].
+template <int DT>
+__device__ __forceinline__ void widen8(const Raw8<DT>& r, float v[8]) {
+  if constexpr (DT == DT_F32) {
+    v[0] = __uint_as_float(r.a.x); v[1] = __uint_as_float(r.a.y);
+    v[2] = __uint_as_float(r.a.z); v[3] = __uint_as_float(r.a.w);
+    v[4] = __uint_as_float(r.b.x); v[5] = __uint_as_float(r.b.y);
+    v[6] = __uint_as_float(r.b.z); v[7] = __uint_as_float(r.b.w);
+  } else if constexpr (DT == DT_BF16) {
+    const uint32_t w[4] = {r.a.x, r.a.y, r.a.z, r.a.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[2 * i] = __uint_as_float(w[i] << 16);             // element 2i: low half
+      v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u); // element 2i+1: high half
+    }
+  } else {
+    const uint32_t w[4] = {r.a.x, r.a.y, r.a.z, r.a.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[2 * i] = f16_bits_to_f32(w[i] & 0xFFFFu);
+      v[2 * i + 1] = f16_bits_to_f32(w[i] >> 16);
+    }
+  }
+}
+
+// One element with bounds handling (partial tiles only).
+template <int DT>
+__device__ __forceinline__ float load1(const void* base, int64_t e) {
+  if constexpr (DT == DT_F32) {
+    return static_cast<const float*>(base)[e];
+  } else if constexpr (DT == DT_BF16) {
+    return __uint_as_float((uint32_t)static_cast<const uint16_t*>(base)[e] << 16);
+  } else {
+    return f16_bits_to_f32(static_cast<const uint16_t*>(base)[e]);
+  }
+}
+
+// ------------------------------------------------------------------ group parameters
+// mn, scale = range / L (RN), inv = L / range (RZ; 0 for a constant group).
+struct GroupParams {
+  float mn, scale, inv;
+};
+
+__device__ __forceinline__ GroupParams group_params(float mn, float mx, float Lf) {
+  GroupParams p;
+  mn = __fadd_rn(mn, 0.0f);  // -0 -> +0
+  mx = __fadd_rn(mx, 0.0f);
+  const float range = __fsub_rn(mx, mn);
+  p.mn = mn;
+  p.scale = __fdiv_rn(range, Lf);
+  p.inv = (range == 0.0f) ? 0.0f : __fdiv_rz(Lf, range);
+  return p;
+}
+
+// ----------------------------------------------------------- stochastic rounding + pack
+// Codes of 8 consecutive elements (chunk), packed LSB-first into BITS*8 bits.
+// q_j = floor(t_j + u_j), t_j = (v_j - mn) * inv, u_j = (2 k_j + 1) 2^-17, where k_j is
+// 16-bit lane j of the chunk's Philox block. Computed as
+//   f = 1 + k 2^-23 (bit pattern 0x3F80_0000 | k, one PRMT)
+//   u = fma(f, 128, 2^-17 - 128)          exact: (2k+1) 2^-17
+//   v = add.rm(t, u)                        floor(v) == floor(t + u) (RD never crosses an integer)
+//   w = add.rm(v, 2^23)                     bits(w) = 0x4B00_0000 + floor(v)   (0 <= v < 2^23)
+// and packed with one IMAD per element: acc += bits(w) << (j BITS) (mod 2^32), minus the
+// constant sum of the 0x4B00_0000 terms.
+template <int BITS>
+struct PackedUnit {
+  uint32_t lo, hi;  // hi used only for BITS == 8 (64-bit unit)
+};
+
+template <int BITS>
+__device__ __forceinline__ constexpr uint32_t magic_sum(int first, int count) {
+  uint32_t s = 0;
+  for (int j = 0; j < count; ++j) s += 0x4B000000u << ((first + j) * BITS);
+  return s;
+}
+
+template <int BITS>
+__device__ __forceinline__ PackedUnit<BITS> quantize_chunk(const float v[8], float mn, float inv,
+                                                           uint4 r) {
+  const f2_t mn2 = f2_make(mn, mn);
+  const f2_t inv2 = f2_make(inv, inv);
+  const f2_t c128 = f2_make(128.0f, 128.0f);
+  const f2_t cu = f2_make(-128.0f + 0x1p-17f, -128.0f + 0x1p-17f);
+  const f2_t magic = f2_make(8388608.0f, 8388608.0f);
+  const uint32_t words[4] = {r.x, r.y, r.z, r.w};
+  uint32_t w[8];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    // elements 2p (low half of Philox word p) and 2p+1 (high half)
+    const f2_t x2 = f2_make(v[2 * p], v[2 * p + 1]);
+    const f2_t t2 = f2_mul_rn(f2_sub_rn(x2, mn2), inv2);
+    const uint32_t flo = __byte_perm(words[p], 0x3F800000u, 0x7610);
+    const uint32_t fhi = __byte_perm(words[p], 0x3F800000u, 0x7632);
+    const f2_t u2 = f2_fma_rn(f2_bits(flo, fhi), c128, cu);
+    const f2_t w2 = f2_add_rm(f2_add_rm(t2, u2), magic);
+    f2_split_bits(w2, w[2 * p], w[2 * p + 1]);
+  }
+  PackedUnit<BITS> out;
+  if constexpr (BITS == 8) {
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) lo += w[j] << (8 * j);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) hi += w[4 + j] << (8 * j);
+    out.lo = lo - magic_sum<8>(0, 4);
+    out.hi = hi - magic_sum<8>(0, 4);
+  } else {
+    uint32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc += w[j] << (BITS * j);
+    out.lo = acc - magic_sum<BITS>(0, 8);
+    out.hi = 0;
+  }
+  return out;
+}
+
+// Store the chunk's packed unit. Element e0 (multiple of 8) starts at bit e0*BITS, a byte
+// boundary; the unit is 8*BITS bits: u8 / u16 / u32 / u64.
+template <int BITS>
+__device__ __forceinline__ void store_unit(uint32_t* packed, int64_t e0, PackedUnit<BITS> u) {
+  unsigned char* bytes = reinterpret_cast<unsigned char*>(packed) + (e0 * BITS) / 8;
+  if constexpr (BITS == 1) {
+    *reinterpret_cast<uint8_t*>(bytes) = (uint8_t)u.lo;
+  } else if constexpr (BITS == 2) {
+    *reinterpret_cast<uint16_t*>(bytes) = (uint16_t)u.lo;
+  } else if constexpr (BITS == 4) {
+    *reinterpret_cast<uint32_t*>(bytes) = u.lo;
+  } else {
+    *reinterpret_cast<uint2*>(bytes) = make_uint2(u.lo, u.hi);
+  }
+}
+
+// Guarded form for a tensor's last (partial) tile: only bytes of words < nwords.
+template <int BITS>
+__device__ __forceinline__ void store_unit_guarded(uint32_t* packed, int64_t e0, int64_t nwords,
+                                                   PackedUnit<BITS> u) {
+  const int64_t byte0 = (e0 * BITS) / 8;
+  if constexpr (BITS == 8) {
+    const int64_t w0 = byte0 / 4;
+    if (w0 < nwords) packed[w0] = u.lo;
+    if (w0 + 1 < nwords) packed[w0 + 1] = u.hi;
+  } else {
+    if (byte0 / 4 < nwords) store_unit<BITS>(packed, e0, u);
+  }
+}
+
+}  // namespace gact

@@ -1,0 +1,63 @@
+// gact_internal.h — parameter blocks shared by the host launchers and the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gact {
+
+constexpr int kMaxBatch = 256;  // == GACT_MAX_BATCH
+
+// One tensor of a quantize launch.
+struct QTensor {
+  const void* x;
+  uint32_t* packed;
+  float* group_min;
+  float* group_scale;
+  int64_t n;
+  int64_t nwords;
+  uint64_t seed;
+};
+
+// Launch parameters (passed by value as __grid_constant__; MAXB = 1 for single calls).
+// Tensors are concatenated in tile space: tensor i owns tiles [tile_start[i], tile_start[i+1]).
+template <int MAXB>
+struct QBatch {
+  int32_t count;
+  int32_t log2g;    // group size G = 2^log2g, 5 <= log2g <= 12
+  float Lf;         // 2^bits - 1 (used by the stats-only kernel; BITS is a template param otherwise)
+  int64_t tiles_total;
+  int64_t tile_start[MAXB + 1];
+  QTensor t[MAXB];
+};
+
+struct DTensor {
+  void* y;
+  const uint32_t* packed;
+  const float* group_min;
+  const float* group_scale;
+  int64_t n;
+};
+
+template <int MAXB>
+struct DBatch {
+  int32_t count;
+  int32_t log2g;
+  int64_t tiles_total;
+  int64_t tile_start[MAXB + 1];
+  DTensor t[MAXB];
+};
+
+// Host-side launchers (gact_quantize.cu / gact_dequant.cu). Return cudaError_t of the launch.
+// `dtype` in {0,1,2}; `bits` in {1,2,4,8}. Tile sizes: quantize max(G, 256), dequant 256.
+template <int MAXB>
+cudaError_t launch_quantize(const QBatch<MAXB>& p, int dtype, int bits, cudaStream_t s);
+template <int MAXB>
+cudaError_t launch_group_stats(const QBatch<MAXB>& p, int dtype, cudaStream_t s);
+template <int MAXB>
+cudaError_t launch_dequantize(const DBatch<MAXB>& p, int dtype, int bits, cudaStream_t s);
+
+inline int64_t quantize_tile_elems(int log2g) { return log2g >= 8 ? (int64_t(1) << log2g) : 256; }
+constexpr int64_t kDequantTileElems = 256;
+
+}  // namespace gact

@@ -1,0 +1,385 @@
+// gact_quantize.cu — fused group-reduce + stochastic-rounding quantize + bit-pack kernels
+// (steps a1-a3 of DESIGN.md §1; the quantizer of App. Prop. 3), sm_100a.
+//
+// Work decomposition. A tensor of n elements is cut into tiles of TE = max(G, 256)
+// elements; a warp owns a tile at a time and each lane a chunk of 8 consecutive elements
+// (one Philox4x32-10 call = 8 x 16-bit lanes; one 16- or 32-byte coalesced load).
+//  * G >= 256: one tile == one group. The group is reduced in registers (3-input
+//    FMNMX3 in-thread, one CREDUX per warp for min and max), coded from the same
+//    registers and written once: x is read exactly once. U tiles are in flight per warp
+//    (memory-level parallelism), and the two IEEE divisions of the U groups are spread
+//    over U lanes and broadcast back with one shuffle.
+//  * G < 256: a tile holds 256/G groups of G/8 lanes; segmented shuffle reduction.
+//  * G >= 2048: two passes over the group (the second pass hits L2), register-light.
+// Tensors of a batch are concatenated in tile space (QBatch::tile_start); warps walk
+// tiles grid-stride, so the active window of every launch is compact in memory.
+// Each tensor's last tile may be partial (n % TE != 0) and takes a guarded path.
+#include <cfloat>
+
+#include "gact_device.cuh"
+#include "gact_internal.h"
+
+namespace gact {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+template <int MAXB>
+__device__ __forceinline__ int advance_cursor(const QBatch<MAXB>& P, int cur, int64_t tile) {
+  if constexpr (MAXB > 1) {
+    while (cur + 1 < P.count && tile >= P.tile_start[cur + 1]) ++cur;
+  }
+  return cur;
+}
+
+__device__ __forceinline__ void chunk_minmax(const float v[8], float& mn, float& mx) {
+  mn = min3f(min3f(mn, v[0], v[1]), min3f(v[2], v[3], v[4]), min3f(v[5], v[6], v[7]));
+  mx = max3f(max3f(mx, v[0], v[1]), max3f(v[2], v[3], v[4]), max3f(v[5], v[6], v[7]));
+}
+
+template <int DT>
+__device__ __forceinline__ void load8_guarded(float v[8], const void* x, int64_t e, int64_t n,
+                                              float fill) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = (e + j < n) ? load1<DT>(x, e + j) : fill;
+}
+
+// Codes of a chunk whose elements >= n were replaced by mn (t = 0 -> q = 0, the zero
+// padding of the last word).
+template <int DT, int BITS>
+__device__ __forceinline__ void code_chunk_guarded(const QTensor& T, int64_t e, float mn,
+                                                   float inv) {
+  float v[8];
+  load8_guarded<DT>(v, T.x, e, T.n, mn);
+  const uint4 r = philox4x32_10((uint64_t)e >> 3, (uint32_t)T.seed, (uint32_t)(T.seed >> 32));
+  store_unit_guarded<BITS>(T.packed, e, T.nwords, quantize_chunk<BITS>(v, mn, inv, r));
+}
+
+// Last tile of a tensor with G >= 256 (one short group): guarded loads, warp reduction.
+template <int DT, int BITS, bool STATS>
+__device__ void partial_tile_big(const QTensor& T, int64_t e0, int log2g, float Lf, int lane) {
+  const int cpl = 1 << (log2g - 8);
+  float lmn = FLT_MAX, lmx = -FLT_MAX;  // neutral; the tile has at least one element
+  for (int c = 0; c < cpl; ++c) {
+    const int64_t e = e0 + c * kWarpTile + lane * kChunk;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (e + j < T.n) {
+        const float x = load1<DT>(T.x, e + j);
+        lmn = fminf(lmn, x);
+        lmx = fmaxf(lmx, x);
+      }
+    }
+  }
+  const GroupParams gp = group_params(warp_min(lmn), warp_max(lmx), Lf);
+  const int64_t g = e0 >> log2g;
+  if (lane == 0) {
+    T.group_min[g] = gp.mn;
+    T.group_scale[g] = gp.scale;
+  }
+  if constexpr (!STATS) {
+    for (int c = 0; c < cpl; ++c) {
+      const int64_t e = e0 + c * kWarpTile + lane * kChunk;
+      if ((e * BITS) / 32 < T.nwords) code_chunk_guarded<DT, BITS>(T, e, gp.mn, gp.inv);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// G in {256, 512, 1024}: CPL = G/256 chunks per lane kept in registers.
+template <int DT, int BITS, int CPL, int MAXB, bool STATS>
+__global__ void __launch_bounds__(kThreads)
+    quantize_big_kernel(const __grid_constant__ QBatch<MAXB> P) {
+  constexpr int U = CPL == 1 ? 4 : (CPL == 2 ? 2 : 1);
+  constexpr int TE = CPL * kWarpTile;
+  const int lane = threadIdx.x & 31;
+  const int64_t W = (int64_t)gridDim.x * kWarps;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
+  int cur = 0;
+  for (int64_t base = gw; base < P.tiles_total; base += (int64_t)U * W) {
+    int tix[U];
+    int64_t e0[U];
+    bool full[U], valid[U];
+    Raw8<DT> raw[U][CPL];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t tile = base + (int64_t)k * W;
+      valid[k] = tile < P.tiles_total;
+      full[k] = false;
+      tix[k] = cur;
+      e0[k] = 0;
+      if (valid[k]) {
+        cur = advance_cursor(P, cur, tile);
+        tix[k] = cur;
+        e0[k] = (tile - P.tile_start[cur]) * TE;
+        full[k] = e0[k] + TE <= P.t[cur].n;
+        if (full[k]) {
+#pragma unroll
+          for (int c = 0; c < CPL; ++c)
+            load8<DT>(raw[k][c], P.t[cur].x, e0[k] + c * kWarpTile + lane * kChunk);
+        }
+      }
+    }
+    float v[U][CPL][8];
+    float mnk[U], mxk[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      float lmn = FLT_MAX, lmx = -FLT_MAX;
+      if (full[k]) {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          widen8<DT>(raw[k][c], v[k][c]);
+          chunk_minmax(v[k][c], lmn, lmx);
+        }
+      }
+      mnk[k] = warp_min(lmn);
+      mxk[k] = warp_max(lmx);
+    }
+    // The U groups' divisions run on lanes 0..U-1 (lane l handles tile l % U).
+    const int sel = lane & (U - 1);
+    float a = mnk[0], b = mxk[0];
+#pragma unroll
+    for (int k = 1; k < U; ++k) {
+      if (sel == k) {
+        a = mnk[k];
+        b = mxk[k];
+      }
+    }
+    const GroupParams gp = group_params(a, b, Lf);
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      if (full[k]) {
+        const QTensor& T = P.t[tix[k]];
+        const float inv = __shfl_sync(kFull, gp.inv, k);
+        const float mn = __fadd_rn(mnk[k], 0.0f);
+        if (lane == k) {
+          const int64_t g = e0[k] / TE;
+          T.group_min[g] = gp.mn;
+          T.group_scale[g] = gp.scale;
+        }
+        if constexpr (!STATS) {
+          const uint32_t k0 = (uint32_t)T.seed, k1 = (uint32_t)(T.seed >> 32);
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            const int64_t e = e0[k] + c * kWarpTile + lane * kChunk;
+            const uint4 r = philox4x32_10((uint64_t)e >> 3, k0, k1);
+            store_unit<BITS>(T.packed, e, quantize_chunk<BITS>(v[k][c], mn, inv, r));
+          }
+        }
+      } else if (valid[k]) {
+        partial_tile_big<DT, BITS, STATS>(P.t[tix[k]], e0[k], P.log2g, Lf, lane);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// G in {2048, 4096}: two passes over the group (the second is served by L2).
+template <int DT, int BITS, int MAXB, bool STATS>
+__global__ void __launch_bounds__(kThreads)
+    quantize_twopass_kernel(const __grid_constant__ QBatch<MAXB> P) {
+  const int lane = threadIdx.x & 31;
+  const int64_t W = (int64_t)gridDim.x * kWarps;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
+  const int cpl = 1 << (P.log2g - 8);
+  const int64_t TE = (int64_t)1 << P.log2g;
+  int cur = 0;
+  for (int64_t tile = gw; tile < P.tiles_total; tile += W) {
+    cur = advance_cursor(P, cur, tile);
+    const QTensor& T = P.t[cur];
+    const int64_t e0 = (tile - P.tile_start[cur]) * TE;
+    if (e0 + TE > T.n) {
+      partial_tile_big<DT, BITS, STATS>(T, e0, P.log2g, Lf, lane);
+      continue;
+    }
+    float lmn = FLT_MAX, lmx = -FLT_MAX;
+    for (int c = 0; c < cpl; c += 4) {
+      Raw8<DT> raw[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) load8<DT>(raw[i], T.x, e0 + (c + i) * kWarpTile + lane * kChunk);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float v[8];
+        widen8<DT>(raw[i], v);
+        chunk_minmax(v, lmn, lmx);
+      }
+    }
+    const GroupParams gp = group_params(warp_min(lmn), warp_max(lmx), Lf);
+    if (lane == 0) {
+      T.group_min[e0 >> P.log2g] = gp.mn;
+      T.group_scale[e0 >> P.log2g] = gp.scale;
+    }
+    if constexpr (!STATS) {
+      const uint32_t k0 = (uint32_t)T.seed, k1 = (uint32_t)(T.seed >> 32);
+      for (int c = 0; c < cpl; c += 4) {
+        Raw8<DT> raw[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) load8<DT>(raw[i], T.x, e0 + (c + i) * kWarpTile + lane * kChunk);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float v[8];
+          widen8<DT>(raw[i], v);
+          const int64_t e = e0 + (c + i) * kWarpTile + lane * kChunk;
+          const uint4 r = philox4x32_10((uint64_t)e >> 3, k0, k1);
+          store_unit<BITS>(T.packed, e, quantize_chunk<BITS>(v, gp.mn, gp.inv, r));
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// G in {32, 64, 128}: a 256-element tile holds 256/G groups of lpg = G/8 lanes each.
+template <int DT, int BITS, int MAXB, bool STATS>
+__global__ void __launch_bounds__(kThreads)
+    quantize_small_kernel(const __grid_constant__ QBatch<MAXB> P) {
+  constexpr int U = 4;
+  const int lane = threadIdx.x & 31;
+  const int64_t W = (int64_t)gridDim.x * kWarps;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
+  const int lpg = 1 << (P.log2g - 3);  // lanes per group
+  int cur = 0;
+  for (int64_t base = gw; base < P.tiles_total; base += (int64_t)U * W) {
+    int tix[U];
+    int64_t e[U];
+    bool full[U], valid[U];
+    Raw8<DT> raw[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t tile = base + (int64_t)k * W;
+      valid[k] = tile < P.tiles_total;
+      full[k] = false;
+      tix[k] = cur;
+      e[k] = 0;
+      if (valid[k]) {
+        cur = advance_cursor(P, cur, tile);
+        tix[k] = cur;
+        const int64_t t0 = (tile - P.tile_start[cur]) * kWarpTile;
+        e[k] = t0 + lane * kChunk;
+        full[k] = t0 + kWarpTile <= P.t[cur].n;
+        if (full[k]) load8<DT>(raw[k], P.t[cur].x, e[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      if (!valid[k]) continue;
+      const QTensor& T = P.t[tix[k]];
+      float v[8];
+      float lmn = FLT_MAX, lmx = -FLT_MAX;
+      if (full[k]) {
+        widen8<DT>(raw[k], v);
+        chunk_minmax(v, lmn, lmx);
+      } else {
+        load8_guarded<DT>(v, T.x, e[k], T.n, FLT_MAX);
+        lmn = min3f(min3f(v[0], v[1], v[2]), min3f(v[3], v[4], v[5]), fminf(v[6], v[7]));
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (e[k] + j < T.n) lmx = fmaxf(lmx, v[j]);
+      }
+      for (int o = 1; o < lpg; o <<= 1) {
+        lmn = fminf(lmn, __shfl_xor_sync(kFull, lmn, o));
+        lmx = fmaxf(lmx, __shfl_xor_sync(kFull, lmx, o));
+      }
+      const int64_t g = e[k] >> P.log2g;
+      const int64_t g_first_elem = g << P.log2g;
+      if (g_first_elem >= T.n) continue;  // group entirely beyond the tensor
+      const GroupParams gp = group_params(lmn, lmx, Lf);
+      if ((lane & (lpg - 1)) == 0) {
+        T.group_min[g] = gp.mn;
+        T.group_scale[g] = gp.scale;
+      }
+      if constexpr (!STATS) {
+        if (full[k]) {
+          const uint4 r = philox4x32_10((uint64_t)e[k] >> 3, (uint32_t)T.seed, (uint32_t)(T.seed >> 32));
+          store_unit<BITS>(T.packed, e[k], quantize_chunk<BITS>(v, gp.mn, gp.inv, r));
+        } else if ((e[k] * BITS) / 32 < T.nwords) {
+          code_chunk_guarded<DT, BITS>(T, e[k], gp.mn, gp.inv);
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------- launching
+template <typename K>
+int max_blocks_per_sm(K kernel) {
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreads, 0) != cudaSuccess || b < 1) b = 1;
+  return b;
+}
+
+inline int sm_count() {
+  int dev = 0, n = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+template <auto Kernel, typename PB>
+cudaError_t launch_persistent(const PB& p, int64_t tiles_per_warp_iter, cudaStream_t s) {
+  static const int per_sm = max_blocks_per_sm(Kernel);  // one cache per kernel
+  const int64_t want = (p.tiles_total + (int64_t)kWarps * tiles_per_warp_iter - 1) /
+                       ((int64_t)kWarps * tiles_per_warp_iter);
+  const int64_t cap = (int64_t)sm_count() * per_sm;
+  const int grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
+  Kernel<<<grid, kThreads, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <int DT, int BITS, int MAXB, bool STATS>
+cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
+  switch (p.log2g) {
+    case 5: case 6: case 7:
+      return launch_persistent<quantize_small_kernel<DT, BITS, MAXB, STATS>>(p, 4, s);
+    case 8:
+      return launch_persistent<quantize_big_kernel<DT, BITS, 1, MAXB, STATS>>(p, 4, s);
+    case 9:
+      return launch_persistent<quantize_big_kernel<DT, BITS, 2, MAXB, STATS>>(p, 2, s);
+    case 10:
+      return launch_persistent<quantize_big_kernel<DT, BITS, 4, MAXB, STATS>>(p, 1, s);
+    default:
+      return launch_persistent<quantize_twopass_kernel<DT, BITS, MAXB, STATS>>(p, 1, s);
+  }
+}
+
+template <int DT, int MAXB>
+cudaError_t launch_q_bits(const QBatch<MAXB>& p, int bits, cudaStream_t s) {
+  switch (bits) {
+    case 1: return launch_q<DT, 1, MAXB, false>(p, s);
+    case 2: return launch_q<DT, 2, MAXB, false>(p, s);
+    case 4: return launch_q<DT, 4, MAXB, false>(p, s);
+    default: return launch_q<DT, 8, MAXB, false>(p, s);
+  }
+}
+
+}  // namespace
+
+template <int MAXB>
+cudaError_t launch_quantize(const QBatch<MAXB>& p, int dtype, int bits, cudaStream_t s) {
+  if (p.tiles_total == 0) return cudaSuccess;
+  switch (dtype) {
+    case DT_F32: return launch_q_bits<DT_F32, MAXB>(p, bits, s);
+    case DT_BF16: return launch_q_bits<DT_BF16, MAXB>(p, bits, s);
+    default: return launch_q_bits<DT_F16, MAXB>(p, bits, s);
+  }
+}
+
+template <int MAXB>
+cudaError_t launch_group_stats(const QBatch<MAXB>& p, int dtype, cudaStream_t s) {
+  if (p.tiles_total == 0) return cudaSuccess;
+  switch (dtype) {
+    case DT_F32: return launch_q<DT_F32, 1, MAXB, true>(p, s);
+    case DT_BF16: return launch_q<DT_BF16, 1, MAXB, true>(p, s);
+    default: return launch_q<DT_F16, 1, MAXB, true>(p, s);
+  }
+}
+
+template cudaError_t launch_quantize<1>(const QBatch<1>&, int, int, cudaStream_t);
+template cudaError_t launch_quantize<kMaxBatch>(const QBatch<kMaxBatch>&, int, int, cudaStream_t);
+template cudaError_t launch_group_stats<1>(const QBatch<1>&, int, cudaStream_t);
+
+}  // namespace gact

@@ -176,6 +176,15 @@ def make_tensor(spec: TensorSpec, seed: int, device="cpu", dtype=torch.float32) 
     return x.to(dtype)
 
 
+def make_sample(spec: TensorSpec, seed: int, limit: int, dtype=torch.float32) -> torch.Tensor:
+    """The first `limit` elements (flattened) of a tensor drawn like `spec` but with the
+    leading (batch) dimension cut to what `limit` needs: a bounded CPU sample."""
+    per_row = max(1, spec.numel // spec.shape[0])
+    rows = min(spec.shape[0], -(-limit // per_row))
+    small = TensorSpec(spec.name, (rows,) + tuple(spec.shape[1:]), spec.kind)
+    return make_tensor(small, seed, "cpu", dtype).reshape(-1)[:limit]
+
+
 def c1_tensor(bits: int = 2, G: int = 256, n: int = 4096, seed: int = DATA_SEED) -> np.ndarray:
     """C1: n fp32 values N(0,1); group 3 constant; group 5 on an exact b-bit grid
     (x = m0 + k 2^e with k in [0, 2^b - 1] and both ends present)."""

@@ -1,0 +1,129 @@
+"""The C-ABI library without a GPU: it loads, exports every symbol include/gact.h declares,
+its host-only logic (sizes, status strings, argument validation, the bit allocator) is
+right, and device calls fail loudly (GACT_ERR_CUDA) instead of falling back to the CPU."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2206_11357_b200 as gact
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "gact.h")
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not os.path.exists(gact.LIB_PATH):
+        subprocess.run(["make", "-j8", "lib"], cwd=ROOT, check=True)
+    return gact.lib()
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(gact_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(L):
+    names = _declared()
+    assert len(names) >= 10
+    out = subprocess.run(["nm", "-D", "--defined-only", gact.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (gact_\w+)", out))
+    missing = [n for n in names if n not in exported]
+    assert not missing, missing
+    for n in names:
+        assert getattr(L, n) is not None
+
+
+def test_no_oracle_linkage():
+    """The product library neither links nor references the oracle."""
+    out = subprocess.run(["nm", "-D", gact.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    assert "oracle" not in out
+    ldd = subprocess.run(["ldd", gact.LIB_PATH], capture_output=True, text=True).stdout
+    assert "oracle" not in ldd
+
+
+def test_sizes_and_strings(L):
+    assert L.gact_version() >> 16 == 1
+    assert gact.num_groups(4096, 256) == 16 and gact.num_groups(4097, 256) == 17
+    assert gact.num_groups(0, 256) == 0 and L.gact_num_groups(-1, 256) == -1
+    assert gact.packed_words(4096, 2) == 256 and gact.packed_words(5, 1) == 1
+    assert gact.packed_words(33, 8) == 9 and L.gact_packed_words(5, 0) == -1
+    for s, name in enumerate(["GACT_OK", "GACT_ERR_INVALID_ARG", "GACT_ERR_UNSUPPORTED_BITS",
+                              "GACT_ERR_GROUP_SIZE", "GACT_ERR_ALIGNMENT", "GACT_ERR_INFEASIBLE",
+                              "GACT_ERR_CUDA"]):
+        assert L.gact_status_string(s).decode() == name
+
+
+A = 0x10000  # a 16-byte-aligned fake device address: validation never dereferences
+
+
+@pytest.mark.parametrize("args,expect", [
+    (dict(bits=3), 2), (dict(bits=0), 2), (dict(bits=16), 2),
+    (dict(G=100), 3), (dict(G=16), 3), (dict(G=8192), 3), (dict(G=48), 3),
+    (dict(x=A + 8), 4), (dict(packed=A + 4), 4), (dict(mn=A + 2), 4),
+    (dict(n=-1), 1), (dict(dtype=3), 1), (dict(x=0), 1),
+])
+def test_quantize_validation(L, args, expect):
+    a = dict(x=A, dtype=1, n=1000, G=256, bits=2, packed=A, mn=A, sc=A)
+    a.update(args)
+    st = L.gact_quantize_pack(a["x"], a["dtype"], a["n"], a["G"], a["bits"], 1, a["packed"], a["mn"], a["sc"], None)
+    assert st == expect
+
+
+def test_dequantize_validation(L):
+    assert L.gact_unpack_dequantize(A, A, A, 10, 256, 3, A, 0, None) == 2
+    assert L.gact_unpack_dequantize(A, A, A, 10, 96, 2, A, 0, None) == 3
+    assert L.gact_unpack_dequantize(A, A, A, 10, 256, 2, A + 4, 0, None) == 4
+    assert L.gact_unpack_dequantize(A, A, A, 10, 256, 2, A, 7, None) == 1
+    assert L.gact_group_stats(A, 0, 10, 256, 5, A, A, None) == 2
+
+
+def test_empty_is_a_no_op(L):
+    assert L.gact_quantize_pack(0, 0, 0, 256, 2, 1, 0, 0, 0, None) == 0
+    assert L.gact_unpack_dequantize(0, 0, 0, 0, 256, 2, 0, 0, None) == 0
+    assert L.gact_quantize_pack_batch(None, 0, 256, None) == 0
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
+def test_device_call_without_gpu_fails_loudly(L):
+    st = L.gact_quantize_pack(A, 1, 4096, 256, 2, 1, A, A, A, None)
+    assert st == 6  # GACT_ERR_CUDA, never a silent CPU fallback
+    with pytest.raises(ValueError):
+        gact.quantize_pack(torch.zeros(256, dtype=torch.bfloat16), 2, 1)
+
+
+# ---------------------------------------------------------------- host allocator parity
+def test_allocator_matches_oracle(L, orc):
+    rng = np.random.default_rng(3)
+    for ladder in ([1, 2, 4, 8], [1, 2, 4, 8, 32], [2, 3, 4, 8], [4]):
+        for _ in range(300):
+            Lt = int(rng.integers(1, 40))
+            D = rng.integers(1, 10**6, size=Lt).astype(np.int64)
+            c = 10.0 ** rng.uniform(-6, 6, size=Lt)
+            c[rng.random(Lt) < 0.1] = 0.0
+            B = int(rng.integers(ladder[0] * D.sum(), ladder[-1] * D.sum() + 1))
+            rc, ref = orc.allocate_bits(c, D, ladder, B)
+            assert rc == 0
+            got = gact.allocate_bits(c, D, B, ladder)
+            assert np.array_equal(got, ref)
+
+
+def test_allocator_ties_and_errors(L, orc):
+    c = np.ones(50)
+    D = np.full(50, 7, dtype=np.int64)
+    for B in range(50 * 7, 8 * 50 * 7 + 1, 97):
+        assert np.array_equal(gact.allocate_bits(c, D, B), orc.allocate_bits(c, D, [1, 2, 4, 8], B)[1])
+    with pytest.raises(gact.GactError) as e:
+        gact.allocate_bits([1.0, 1.0], [10, 10], 19)
+    assert e.value.status == 5
+    with pytest.raises(gact.GactError):
+        gact.allocate_bits([float("nan")], [10], 100)
+    with pytest.raises(gact.GactError):
+        gact.allocate_bits([1.0], [10], 100, ladder=[2, 2])

@@ -1,0 +1,243 @@
+"""GPU parity: the CUDA path (through the C ABI, via the thin binding) against the CPU
+oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star): packed codes, group_min and group_scale BIT-EXACT;
+dequantized values within 1 ulp of the output dtype (fp32 / bf16 / fp16); allocations
+identical (tests/test_abi.py). Sizes span several tiles and a ragged tail; edge cases
+cover empty / tiny / constant / subnormal / signed-zero / exact-grid groups, and every
+group size 32..4096. Full-size workloads are checked on sampled groups in
+tests/test_gpu_fullsize.py.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TAGS = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}
+DTYPES = [torch.float32, torch.bfloat16, torch.float16]
+BITS = [1, 2, 4, 8]
+GROUPS = [32, 64, 128, 256, 512, 1024, 2048, 4096]
+
+
+@pytest.fixture(scope="module")
+def gact():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2206_11357_b200 as g
+    g.lib()
+    return g
+
+
+def host_bits(t: torch.Tensor) -> np.ndarray:
+    """Raw bit patterns of a tensor as a host array (uint32 for fp32, uint16 otherwise)."""
+    t = t.detach().contiguous().cpu()
+    if t.dtype == torch.float32:
+        return t.view(torch.int32).numpy().view(np.uint32).reshape(-1)
+    if t.dtype in (torch.bfloat16, torch.float16):
+        return t.view(torch.int16).numpy().view(np.uint16).reshape(-1)
+    if t.dtype == torch.int32:
+        return t.numpy().view(np.uint32).reshape(-1)
+    raise TypeError(t.dtype)
+
+
+def oracle_input(x: torch.Tensor) -> np.ndarray:
+    b = host_bits(x)
+    return b.view(np.float32) if x.dtype == torch.float32 else b
+
+
+def ulp_distance(a: np.ndarray, b: np.ndarray, width: int) -> np.ndarray:
+    """Distance in representable steps between two arrays of float bit patterns."""
+    a = a.astype(np.int64)
+    b = b.astype(np.int64)
+    sign = 1 << (width - 1)
+    mag = sign - 1
+
+    def key(v):
+        return np.where(v & sign, -(v & mag), v & mag)
+    return np.abs(key(a) - key(b))
+
+
+def check_quantize(gact, orc, x: torch.Tensor, G: int, bits: int, seed: int):
+    ct = gact.quantize_pack(x, bits, seed, G)
+    torch.cuda.synchronize()
+    ref_p, ref_mn, ref_sc = orc.quantize_pack(oracle_input(x), TAGS[x.dtype], G, bits, seed)
+    got_p = host_bits(ct.packed)
+    assert got_p.size == ref_p.size
+    bad = np.nonzero(got_p != ref_p)[0]
+    assert bad.size == 0, f"{bad.size} packed words differ, first at word {bad[:5]}"
+    assert np.array_equal(host_bits(ct.group_min), ref_mn.view(np.uint32))
+    assert np.array_equal(host_bits(ct.group_scale), ref_sc.view(np.uint32))
+    return ct, (ref_p, ref_mn, ref_sc)
+
+
+def check_dequantize(gact, orc, ct, ref, n, G, bits, dtype):
+    ref_p, ref_mn, ref_sc = ref
+    y = gact.unpack_dequantize(ct.packed, ct.group_min, ct.group_scale, n, bits, G, dtype)
+    torch.cuda.synchronize()
+    ref_y = orc.unpack_dequantize(ref_p, ref_mn, ref_sc, n, G, bits, TAGS[dtype])
+    d = ulp_distance(host_bits(y), ref_y, 32 if dtype == torch.float32 else 16)
+    assert d.max(initial=0) <= 1, f"max ulp distance {d.max()}"
+    return int((d != 0).sum())
+
+
+def make_input(n, dtype, seed, kind="normal"):
+    rng = np.random.default_rng(seed)
+    v = rng.standard_normal(n) * 10.0 ** rng.uniform(-2, 2)
+    if kind == "mixed" and n > 0:
+        G = 256
+        ng = (n + G - 1) // G
+        for g in range(ng):
+            sl = slice(g * G, min(n, (g + 1) * G))
+            r = g % 6
+            if r == 1:
+                v[sl] = 3.25  # constant group
+            elif r == 2:
+                v[sl] = synth.exact_grid_group(G, 2, rng)[: v[sl].size]
+            elif r == 3:
+                v[sl] = rng.integers(0, 5, v[sl].size) * 2.0 ** -149  # subnormal range
+            elif r == 4:
+                v[sl] = np.where(rng.random(v[sl].size) < 0.5, -0.0, 0.0)  # signed zeros only
+            elif r == 5:
+                v[sl] = rng.standard_normal(v[sl].size) * 1e30
+    t = torch.from_numpy(v.astype(np.float32)).to(dtype)
+    return t.cuda()
+
+
+# ----------------------------------------------------------------------------- configs
+def test_c1_config(gact, orc):
+    """configs[0]: 4096 fp32, G=256, b=2, fixed seed (plus a constant and a grid group)."""
+    x = torch.from_numpy(synth.c1_tensor(2, 256)).cuda()
+    ct, ref = check_quantize(gact, orc, x, 256, 2, 0x5EED)
+    assert check_dequantize(gact, orc, ct, ref, x.numel(), 256, 2, torch.float32) == 0
+    # exact-grid group decodes bit-exactly (B3 on the grid)
+    y = ct.decompress()
+    assert torch.equal(y[5 * 256: 6 * 256], x[5 * 256: 6 * 256])
+    assert torch.equal(y[3 * 256: 4 * 256], x[3 * 256: 4 * 256])
+
+
+@pytest.mark.parametrize("dtype", DTYPES, ids=["f32", "bf16", "f16"])
+@pytest.mark.parametrize("bits", BITS)
+@pytest.mark.parametrize("G", GROUPS)
+def test_quantize_dequantize_parity(gact, orc, dtype, bits, G):
+    TE = max(G, 256)
+    n = 3 * TE + 8 * 5 + 3  # several tiles, a ragged tail, a partial chunk
+    x = make_input(n, dtype, seed=G * 10 + bits)
+    ct, ref = check_quantize(gact, orc, x, G, bits, seed=0xABCDEF0123456789 ^ (G * bits))
+    for ydt in DTYPES:
+        check_dequantize(gact, orc, ct, ref, n, G, bits, ydt)
+
+
+@pytest.mark.parametrize("dtype", DTYPES, ids=["f32", "bf16", "f16"])
+@pytest.mark.parametrize("bits", BITS)
+def test_edge_values(gact, orc, dtype, bits):
+    """Constant groups, exact grids, subnormal ranges, signed zeros, 1e30 magnitudes."""
+    n = 256 * 12 + 5
+    x = make_input(n, dtype, seed=bits, kind="mixed")
+    ct, ref = check_quantize(gact, orc, x, 256, bits, seed=bits * 1000003)
+    assert check_dequantize(gact, orc, ct, ref, n, 256, bits, dtype) >= 0
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 8, 9, 31, 33, 255, 256, 257, 511, 1023, 1025])
+@pytest.mark.parametrize("G", [32, 256, 2048])
+def test_tiny_and_ragged_sizes(gact, orc, n, G):
+    for bits in BITS:
+        x = make_input(n, torch.bfloat16, seed=n + bits)
+        ct, ref = check_quantize(gact, orc, x, G, bits, seed=n * 31 + bits)
+        check_dequantize(gact, orc, ct, ref, n, G, bits, torch.float32)
+
+
+def test_empty(gact):
+    x = torch.empty(0, device="cuda", dtype=torch.bfloat16)
+    ct = gact.quantize_pack(x, 2, 1)
+    assert ct.packed.numel() == 0 and ct.group_min.numel() == 0
+    y = ct.decompress()
+    assert y.numel() == 0
+
+
+def test_padding_words_are_zero(gact):
+    """The unused high bits of the last packed word are zero (include/gact.h)."""
+    for bits in BITS:
+        for n in [1, 3, 5, 9, 17, 100]:
+            x = make_input(n, torch.float32, seed=n)
+            ct = gact.quantize_pack(x, bits, 7, 32)
+            last = int(host_bits(ct.packed)[-1])
+            used = n * bits - 32 * (ct.packed.numel() - 1)
+            if used < 32:
+                assert last >> used == 0
+
+
+@pytest.mark.parametrize("G", [32, 256, 1024, 4096])
+def test_group_stats_matches(gact, orc, G):
+    for dtype in DTYPES:
+        x = make_input(5 * max(G, 256) + 77, dtype, seed=G)
+        for bits in BITS:
+            mn, sc = gact.group_stats(x, bits, G)
+            ct = gact.quantize_pack(x, bits, 3, G)
+            rmn, rsc = orc.group_stats(oracle_input(x), TAGS[dtype], G, bits)
+            assert np.array_equal(host_bits(mn), rmn.view(np.uint32))
+            assert np.array_equal(host_bits(sc), rsc.view(np.uint32))
+            assert torch.equal(mn, ct.group_min) and torch.equal(sc, ct.group_scale)
+
+
+def test_determinism_and_streams(gact):
+    x = make_input(1 << 20, torch.bfloat16, seed=5)
+    a = gact.quantize_pack(x, 4, 99)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        b = gact.quantize_pack(x, 4, 99)
+    s.synchronize()
+    torch.cuda.synchronize()
+    assert torch.equal(a.packed, b.packed) and torch.equal(a.group_scale, b.group_scale)
+    c = gact.quantize_pack(x, 4, 100)
+    assert not torch.equal(a.packed, c.packed)
+
+
+@pytest.mark.parametrize("G", [64, 256, 1024])
+def test_batch_equals_single(gact, G):
+    """Batched launches (mixed dtypes and bits, > GACT_MAX_BATCH tensors) give results
+    identical to one call per tensor."""
+    rng = np.random.default_rng(G)
+    xs, bits, seeds = [], [], []
+    for i in range(300):
+        n = int(rng.integers(1, 3000)) if i % 3 else int(rng.integers(1, 70000))
+        dt = DTYPES[i % 3]
+        xs.append(make_input(n, dt, seed=i))
+        bits.append(BITS[int(rng.integers(0, 4))])
+        seeds.append(synth.tensor_seed(11, i))
+    batch = gact.quantize_pack_batch(xs, bits, seeds, G)
+    ys = gact.unpack_dequantize_batch(batch)
+    torch.cuda.synchronize()
+    for x, b, s, ct, y in zip(xs, bits, seeds, batch, ys):
+        single = gact.quantize_pack(x, b, s, G)
+        assert torch.equal(ct.packed, single.packed)
+        assert torch.equal(ct.group_min, single.group_min)
+        assert torch.equal(ct.group_scale, single.group_scale)
+        assert torch.equal(y.view(-1), single.decompress().view(-1))
+
+
+def test_unbiased_on_gpu(gact, orc):
+    """E[Q(x)] = x: 20000 seeds over the C1 tensor; the GPU mean of the decoded
+    values is within 4 sigma (+ the 2^-17 lane bias) of mn + t * scale, with t the
+    oracle's binary32 transform, and of x itself up to the transform's rounding."""
+    G, bits, N = 256, 2, 20000
+    xh = synth.c1_tensor(bits, G)[:1024]
+    x = torch.from_numpy(xh).cuda()
+    acc = torch.zeros(x.numel(), dtype=torch.float64, device="cuda")
+    acc2 = torch.zeros_like(acc)
+    for s in range(N):
+        y = gact.quantize_pack(x, bits, s, G).decompress().double()
+        acc += y
+        acc2 += y * y
+    mean = (acc / N).cpu().numpy()
+    var = (acc2 / N).cpu().numpy() - mean ** 2
+    mn, sc = orc.group_stats(xh, 0, G, bits)
+    scale = np.repeat(sc.astype(np.float64), G)[: xh.size]
+    p = np.clip((xh.astype(np.float64) - np.repeat(mn, G)[: xh.size]) / np.maximum(scale, 1e-300) % 1.0, 0, 1)
+    sig = np.sqrt(np.maximum(p * (1 - p), 1e-12) / N) * scale
+    tol = 4 * sig + (2.0 ** -17 + 1e-6) * scale + 4 * np.spacing(np.abs(xh)).astype(np.float64)
+    assert np.all(np.abs(mean - xh) <= tol)
+    # Var[y] <= 1/4 range^2 S(b) = scale^2 / 4 (paper's B2 bound)
+    assert np.all(var <= scale ** 2 / 4 * (1 + 6 / np.sqrt(N)) + 1e-30)
