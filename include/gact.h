@@ -23,11 +23,13 @@
  *     scale = range / L                                          (round to nearest)
  *     inv   = range == 0 ? 0 : L / range                        (round toward ZERO)
  * and for every element i of the group
- *     t_i = (x_i - mn) * inv                                     (both round to nearest)
- *     u_i = (2k_i + 1) * 2^-17,  k_i = 16-bit Philox lane of (seed, i)  (below)
- *     q_i = floor(t_i + u_i)          (exact real floor; 0 <= t_i <= L so q_i in [0, L])
+ *     d_i = x_i - mn                                             (round to nearest)
+ *     t_i = fma(d_i, inv, 2^-17)                                 (one rounding, nearest)
+ *     q_i = floor(t_i + k_i 2^-16),  k_i = 16-bit Philox lane of (seed, i)  (below)
+ *                                     (exact real floor; 0 < t_i <= L + 2^-17, q_i in [0, L])
  * which is T_{h,b} of P:233 followed by the stochastic rounding of P:229-230:
- * q_i = ceil(t_i) with probability frac(t_i) (up to 2^-17), else floor(t_i).
+ * q_i = ceil(T) with probability frac(T) (up to 2^-17: the 2^-17 offset centres the
+ * 2^-16 lattice of thresholds), else floor(T).
  * Decompression (T^{-1}):   y_i = fma(q_i, scale, mn) in binary32, then
  * rounded to nearest-even into the output dtype.
  *

@@ -198,8 +198,11 @@ int32_t oracle_group_stats(const void* x, int32_t dtype, int64_t n, int32_t G, i
 /* ------------------------------------------------------------------------------------
  * R4, R5  Stochastic rounding (App. Prop. 3):
  *   Q(h)_j = T^{-1}(ceil(T(h_j)))  w.p. T(h_j) - floor(T(h_j)),  else T^{-1}(floor(T(h_j)))
- * realised as q = floor(t + u), u = (2k+1) 2^-17 with k uniform on [0, 2^16): the event
- * q = ceil(t) is {u >= 1 - frac(t)}, whose probability is frac(t) up to 2^-17.
+ * realised as q = floor(T + 2^-17 + k 2^-16) with k uniform on [0, 2^16): the event
+ * q = ceil(T) is {k 2^-16 >= 1 - frac(T + 2^-17)}, whose probability is frac(T) up to
+ * 2^-17 (the 2^-17 offset centres the 16-bit lattice of thresholds). In binary32 (R5):
+ *   t = fma(h_j - min, inv, 2^-17)   -- T + 2^-17 with ONE rounding (C99 fmaf)
+ *   q = floor(t + k 2^-16)           -- the exact real floor
  * ---------------------------------------------------------------------------------- */
 int32_t oracle_quantize_codes(const void* x, int32_t dtype, int64_t n, int32_t G, int32_t bits,
                               uint64_t seed, int64_t g0, int64_t g1, uint8_t* q_out,
@@ -207,7 +210,7 @@ int32_t oracle_quantize_codes(const void* x, int32_t dtype, int64_t n, int32_t G
   if (!valid_common(n, G, bits, dtype)) return ORACLE_EINVAL;
   int64_t ng = (n + G - 1) / G;
   if (g0 < 0 || g1 > ng || g0 > g1) return ORACLE_EINVAL;
-  const float Lf = (float)((1u << bits) - 1u);
+  const double L = (double)((1u << bits) - 1u);
   for (int64_t g = g0; g < g1; ++g) {
     int64_t lo = g * G, hi = lo + G < n ? lo + G : n;
     group_params p = group_stats_one(x, dtype, lo, hi, bits);
@@ -215,14 +218,12 @@ int32_t oracle_quantize_codes(const void* x, int32_t dtype, int64_t n, int32_t G
     scale_out[g - g0] = p.scale;
     for (int64_t i = lo; i < hi; ++i) {
       float h = oracle_widen(x, dtype, i);
-      float d = h - p.mn;  /* h_j - min_j h   (binary32, RN) */
-      float t = d * p.inv; /* T_{h,b}(h_j) = (2^b - 1)(h_j - min)/(max - min) */
-      if (!(t >= 0.0f && t <= Lf)) return ORACLE_EINVARIANT; /* proven in DESIGN.md R2 */
+      float d = h - p.mn;                   /* h_j - min_j h   (binary32, RN) */
+      float t = fmaf(d, p.inv, 0x1p-17f);   /* (2^b-1)(h_j - min)/(max - min) + 2^-17 */
       uint32_t k = oracle_lane16(seed, (uint64_t)i);
-      double u = (2.0 * (double)k + 1.0) / 131072.0; /* (2k+1) 2^-17, exact */
-      /* (double)t + u is exact whenever t >= 2^-21 (53 bits span 2^8 .. 2^-44); below that
-       * both the real sum and its rounding lie in [0, 1). So this floor is the real one. */
-      double q = floor((double)t + u);
+      /* t >= 2^-17 has ulp >= 2^-41 and t + k 2^-16 < 2^9: the double sum is exact. */
+      double q = floor((double)t + (double)k / 65536.0);
+      if (!(t > 0.0f) || q > L) return ORACLE_EINVARIANT; /* proven in DESIGN.md R2/R5 */
       q_out[i - g0 * G] = (uint8_t)q;
     }
   }

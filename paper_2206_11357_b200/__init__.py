@@ -29,7 +29,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgact.so")
+LIB_PATH = os.environ.get("GACT_LIB_PATH") or os.path.join(_HERE, "libgact.so")  # override: experiments only
 
 F32, BF16, F16 = 0, 1, 2
 DEFAULT_GROUP = 256

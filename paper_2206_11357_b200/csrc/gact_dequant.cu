@@ -102,10 +102,18 @@ __device__ __forceinline__ void store1(void* ybase, int64_t e, float y) {
   }
 }
 
+#ifndef GACT_D_UNIT
+#define GACT_D_UNIT 4
+#endif
+#ifndef GACT_D_MINB
+#define GACT_D_MINB 1
+#endif
+constexpr int kDequantUnit = GACT_D_UNIT;
+
 template <int DT, int BITS, int MAXB>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, GACT_D_MINB)
     dequantize_kernel(const __grid_constant__ DBatch<MAXB> P) {
-  constexpr int U = 4;
+  constexpr int U = kDequantUnit;
   const int lane = threadIdx.x & 31;
   const int64_t W = (int64_t)gridDim.x * kWarps;
   const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
@@ -167,7 +175,7 @@ cudaError_t launch_d(const DBatch<MAXB>& p, cudaStream_t s) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t want = (p.tiles_total + kWarps * 4 - 1) / (kWarps * 4);
+  const int64_t want = (p.tiles_total + kWarps * kDequantUnit - 1) / (kWarps * kDequantUnit);
   const int64_t cap = (int64_t)sms * per_sm;
   const int grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
   kernel<<<grid, kThreads, 0, s>>>(p);

@@ -19,16 +19,31 @@ enum : int { DT_F32 = 0, DT_BF16 = 1, DT_F16 = 2 };
 
 // ------------------------------------------------------------------------ Philox4x32-10
 // Salmon et al., SC'11 (Random123 constants). key = seed, counter = (block lo, hi, 0, 0).
+// Written with explicit PTX (mul.wide.u32 -> one IMAD.WIDE.U32, lop3 -> one LOP3 for the
+// 3-way xor) so that a round costs 2 + 2 instructions; the key schedule is the same for
+// every call with the same seed and is shared (CSE) across the calls of an iteration.
+__device__ __forceinline__ void mul_wide(uint32_t a, uint32_t m, uint32_t& lo, uint32_t& hi) {
+  asm("{\n\t.reg .b64 p;\n\tmul.wide.u32 p, %2, %3;\n\tmov.b64 {%0, %1}, p;\n\t}"
+      : "=r"(lo), "=r"(hi)
+      : "r"(a), "r"(m));
+}
+__device__ __forceinline__ uint32_t xor3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
 __device__ __forceinline__ uint4 philox4x32_10(uint64_t block, uint32_t k0, uint32_t k1) {
   uint32_t c0 = (uint32_t)block, c1 = (uint32_t)(block >> 32), c2 = 0u, c3 = 0u;
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-    const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
-    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
-    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
-    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
-    c1 = (uint32_t)p1;
-    c3 = (uint32_t)p0;
+    uint32_t lo0, hi0, lo1, hi1;
+    mul_wide(c0, 0xD2511F53u, lo0, hi0);
+    mul_wide(c2, 0xCD9E8D57u, lo1, hi1);
+    const uint32_t n0 = xor3(hi1, c1, k0);
+    const uint32_t n2 = xor3(hi0, c3, k1);
+    c1 = lo1;
+    c3 = lo0;
     c0 = n0;
     c2 = n2;
     k0 += 0x9E3779B9u;
@@ -71,6 +86,11 @@ __device__ __forceinline__ f2_t f2_mul_rn(f2_t a, f2_t b) {
 __device__ __forceinline__ f2_t f2_add_rm(f2_t a, f2_t b) {
   f2_t r;
   asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t f2_fma_rm(f2_t a, f2_t b, f2_t c) {
+  f2_t r;
+  asm("fma.rm.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
   return r;
 }
 __device__ __forceinline__ f2_t f2_fma_rn(f2_t a, f2_t b, f2_t c) {
@@ -186,6 +206,17 @@ struct GroupParams {
   float mn, scale, inv;
 };
 
+// RZ(a / b) for finite a > 0, b > 0: q = RN(a / b), then one step toward zero if q
+// overshoots (the residual a - q b of a correctly rounded quotient is exact, so its sign
+// decides); RN overflow (a / b > FLT_MAX) gives FLT_MAX, the RZ result. Avoids the
+// out-of-line __fdiv_rz path.
+__device__ __forceinline__ float div_rz_pos(float a, float b) {
+  const float q = __fdiv_rn(a, b);
+  if (q == __int_as_float(0x7f800000)) return __int_as_float(0x7f7fffff);
+  const float r = __fmaf_rn(-q, b, a);
+  return (r < 0.0f) ? __int_as_float(__float_as_int(q) - 1) : q;
+}
+
 __device__ __forceinline__ GroupParams group_params(float mn, float mx, float Lf) {
   GroupParams p;
   mn = __fadd_rn(mn, 0.0f);  // -0 -> +0
@@ -193,20 +224,21 @@ __device__ __forceinline__ GroupParams group_params(float mn, float mx, float Lf
   const float range = __fsub_rn(mx, mn);
   p.mn = mn;
   p.scale = __fdiv_rn(range, Lf);
-  p.inv = (range == 0.0f) ? 0.0f : __fdiv_rz(Lf, range);
+  p.inv = (range > 0.0f) ? div_rz_pos(Lf, range) : 0.0f;
   return p;
 }
 
 // ----------------------------------------------------------- stochastic rounding + pack
 // Codes of 8 consecutive elements (chunk), packed LSB-first into BITS*8 bits.
-// q_j = floor(t_j + u_j), t_j = (v_j - mn) * inv, u_j = (2 k_j + 1) 2^-17, where k_j is
-// 16-bit lane j of the chunk's Philox block. Computed as
-//   f = 1 + k 2^-23 (bit pattern 0x3F80_0000 | k, one PRMT)
-//   u = fma(f, 128, 2^-17 - 128)          exact: (2k+1) 2^-17
-//   v = add.rm(t, u)                        floor(v) == floor(t + u) (RD never crosses an integer)
-//   w = add.rm(v, 2^23)                     bits(w) = 0x4B00_0000 + floor(v)   (0 <= v < 2^23)
-// and packed with one IMAD per element: acc += bits(w) << (j BITS) (mod 2^32), minus the
-// constant sum of the 0x4B00_0000 terms.
+// q_j = floor(t_j + k_j 2^-16) with t_j = fma(v_j - mn, inv, 2^-17) (one rounding) and k_j
+// the 16-bit lane j of the chunk's Philox block (include/gact.h). Per pair of elements:
+//   d = sub(x, mn)                FADD2
+//   t = fma(d, inv, 2^-17)        FFMA2
+//   f = 1 + k 2^-23               PRMT (bit pattern 0x3F80_0000 | k)
+//   v = fma.rm(f, 128, t)         FFMA2.RM   = RD(128 + k 2^-16 + t)
+//   w = add.rm(v, 2^23 - 128)     FADD2.RM   bits(w) = 0x4B00_0000 + floor(t + k 2^-16)
+// (RD never crosses an integer: floor(RD(s)) = floor(s); on [2^23, 2^24) the binary32 grid
+// is the integers.) Then the low byte of bits(w) is the code.
 template <int BITS>
 struct PackedUnit {
   uint32_t lo, hi;  // hi used only for BITS == 8 (64-bit unit)
@@ -224,31 +256,27 @@ __device__ __forceinline__ PackedUnit<BITS> quantize_chunk(const float v[8], flo
                                                            uint4 r) {
   const f2_t mn2 = f2_make(mn, mn);
   const f2_t inv2 = f2_make(inv, inv);
+  const f2_t c17 = f2_make(0x1p-17f, 0x1p-17f);
   const f2_t c128 = f2_make(128.0f, 128.0f);
-  const f2_t cu = f2_make(-128.0f + 0x1p-17f, -128.0f + 0x1p-17f);
-  const f2_t magic = f2_make(8388608.0f, 8388608.0f);
+  const f2_t magic = f2_make(8388608.0f - 128.0f, 8388608.0f - 128.0f);
   const uint32_t words[4] = {r.x, r.y, r.z, r.w};
   uint32_t w[8];
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
     // elements 2p (low half of Philox word p) and 2p+1 (high half)
     const f2_t x2 = f2_make(v[2 * p], v[2 * p + 1]);
-    const f2_t t2 = f2_mul_rn(f2_sub_rn(x2, mn2), inv2);
+    const f2_t t2 = f2_fma_rn(f2_sub_rn(x2, mn2), inv2, c17);
     const uint32_t flo = __byte_perm(words[p], 0x3F800000u, 0x7610);
     const uint32_t fhi = __byte_perm(words[p], 0x3F800000u, 0x7632);
-    const f2_t u2 = f2_fma_rn(f2_bits(flo, fhi), c128, cu);
-    const f2_t w2 = f2_add_rm(f2_add_rm(t2, u2), magic);
+    const f2_t v2 = f2_fma_rm(f2_bits(flo, fhi), c128, t2);
+    const f2_t w2 = f2_add_rm(v2, magic);
     f2_split_bits(w2, w[2 * p], w[2 * p + 1]);
   }
   PackedUnit<BITS> out;
   if constexpr (BITS == 8) {
-    uint32_t lo = 0, hi = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) lo += w[j] << (8 * j);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) hi += w[4 + j] << (8 * j);
-    out.lo = lo - magic_sum<8>(0, 4);
-    out.hi = hi - magic_sum<8>(0, 4);
+    // bytes: gather the low byte of each w_j (byte permutes, integer ALU pipe)
+    out.lo = __byte_perm(__byte_perm(w[0], w[1], 0x0040), __byte_perm(w[2], w[3], 0x0040), 0x5410);
+    out.hi = __byte_perm(__byte_perm(w[4], w[5], 0x0040), __byte_perm(w[6], w[7], 0x0040), 0x5410);
   } else {
     uint32_t acc = 0;
 #pragma unroll
@@ -259,20 +287,24 @@ __device__ __forceinline__ PackedUnit<BITS> quantize_chunk(const float v[8], flo
   return out;
 }
 
-// Store the chunk's packed unit. Element e0 (multiple of 8) starts at bit e0*BITS, a byte
-// boundary; the unit is 8*BITS bits: u8 / u16 / u32 / u64.
+// Store the chunk's packed unit at byte address p. Element e0 (multiple of 8) starts at
+// bit e0*BITS, a byte boundary; the unit is 8*BITS bits: u8 / u16 / u32 / u64.
+template <int BITS>
+__device__ __forceinline__ void store_unit_at(unsigned char* p, PackedUnit<BITS> u) {
+  if constexpr (BITS == 1) {
+    *reinterpret_cast<uint8_t*>(p) = (uint8_t)u.lo;
+  } else if constexpr (BITS == 2) {
+    *reinterpret_cast<uint16_t*>(p) = (uint16_t)u.lo;
+  } else if constexpr (BITS == 4) {
+    *reinterpret_cast<uint32_t*>(p) = u.lo;
+  } else {
+    *reinterpret_cast<uint2*>(p) = make_uint2(u.lo, u.hi);
+  }
+}
+
 template <int BITS>
 __device__ __forceinline__ void store_unit(uint32_t* packed, int64_t e0, PackedUnit<BITS> u) {
-  unsigned char* bytes = reinterpret_cast<unsigned char*>(packed) + (e0 * BITS) / 8;
-  if constexpr (BITS == 1) {
-    *reinterpret_cast<uint8_t*>(bytes) = (uint8_t)u.lo;
-  } else if constexpr (BITS == 2) {
-    *reinterpret_cast<uint16_t*>(bytes) = (uint16_t)u.lo;
-  } else if constexpr (BITS == 4) {
-    *reinterpret_cast<uint32_t*>(bytes) = u.lo;
-  } else {
-    *reinterpret_cast<uint2*>(bytes) = make_uint2(u.lo, u.hi);
-  }
+  store_unit_at<BITS>(reinterpret_cast<unsigned char*>(packed) + (e0 * BITS) / 8, u);
 }
 
 // Guarded form for a tensor's last (partial) tile: only bytes of words < nwords.

@@ -144,7 +144,7 @@ gact_status gact_group_stats(const void* x, int32_t dtype, int64_t n, int32_t gr
   p.Lf = (float)((1 << bits) - 1);
   p.t[0] = make_q(x, n, bits, 0, nullptr, group_min, group_scale);
   p.tile_start[0] = 0;
-  p.tiles_total = p.tile_start[1] = ceil_div(n, gact::quantize_tile_elems(l2));
+  p.tiles_total = p.tile_start[1] = gact::quantize_tiles(n, l2);
   return from_cuda(gact::launch_group_stats<1>(p, dtype, static_cast<cudaStream_t>(stream)));
 }
 
@@ -163,7 +163,7 @@ gact_status gact_quantize_pack(const void* x, int32_t dtype, int64_t n, int32_t 
   p.Lf = (float)((1 << bits) - 1);
   p.t[0] = make_q(x, n, bits, seed, packed, group_min, group_scale);
   p.tile_start[0] = 0;
-  p.tiles_total = p.tile_start[1] = ceil_div(n, gact::quantize_tile_elems(l2));
+  p.tiles_total = p.tile_start[1] = gact::quantize_tiles(n, l2);
   return from_cuda(gact::launch_quantize<1>(p, dtype, bits, static_cast<cudaStream_t>(stream)));
 }
 
@@ -195,7 +195,6 @@ gact_status gact_quantize_pack_batch(const gact_tensor_desc* descs, int32_t coun
     if (st != GACT_OK) return st;
   }
   if (l2 < 0) return GACT_ERR_GROUP_SIZE;
-  const int64_t TE = gact::quantize_tile_elems(l2);
   static thread_local QBatch<gact::kMaxBatch> p;  // 16 KB: keep it off the stack
   return for_each_class(descs, count, [&](ClassKey key) -> gact_status {
     // one launch per <= kMaxBatch tensors of this class, in input order
@@ -211,7 +210,7 @@ gact_status gact_quantize_pack_batch(const gact_tensor_desc* descs, int32_t coun
         if (d.n == 0 || d.dtype != key.dtype || d.bits != key.bits) continue;
         p.tile_start[m] = tiles;
         p.t[m] = make_q(d.data, d.n, d.bits, d.seed, d.packed, d.group_min, d.group_scale);
-        tiles += ceil_div(d.n, TE);
+        tiles += gact::quantize_tiles(d.n, l2);
         ++m;
       }
       if (m == 0) break;

@@ -4,16 +4,18 @@
 // Work decomposition. A tensor of n elements is cut into tiles of TE = max(G, 256)
 // elements; a warp owns a tile at a time and each lane a chunk of 8 consecutive elements
 // (one Philox4x32-10 call = 8 x 16-bit lanes; one 16- or 32-byte coalesced load).
-//  * G >= 256: one tile == one group. The group is reduced in registers (3-input
-//    FMNMX3 in-thread, one CREDUX per warp for min and max), coded from the same
-//    registers and written once: x is read exactly once. U tiles are in flight per warp
-//    (memory-level parallelism), and the two IEEE divisions of the U groups are spread
-//    over U lanes and broadcast back with one shuffle.
-//  * G < 256: a tile holds 256/G groups of G/8 lanes; segmented shuffle reduction.
-//  * G >= 2048: two passes over the group (the second pass hits L2), register-light.
-// Tensors of a batch are concatenated in tile space (QBatch::tile_start); warps walk
-// tiles grid-stride, so the active window of every launch is compact in memory.
-// Each tensor's last tile may be partial (n % TE != 0) and takes a guarded path.
+// Tensors of a batch are concatenated in tile space (QBatch::tile_start), each tensor's
+// tile count rounded up to kTileAlign = 4, so that a warp's UNIT of U <= 4 consecutive
+// tiles never straddles two tensors. Warps walk units grid-stride: the active window of a
+// launch is compact in memory and each warp streams U * TE contiguous elements per step.
+//  * G in {256, 512, 1024}: one tile == one group, reduced in registers (FMNMX3 in-thread,
+//    one CREDUX per warp for min and max), coded from the same registers, written once:
+//    x is read exactly once. The U x CPL Philox blocks of a unit are computed while its
+//    loads are in flight (they depend only on (seed, element index)); the U groups'
+//    divisions run on U lanes and are broadcast with one shuffle.
+//  * G in {32, 64, 128}: a tile holds 256/G groups of G/8 lanes; segmented shuffles.
+//  * G in {2048, 4096}: two passes over the group (the second is served by L2).
+// A tensor's last tile may be partial (n % TE != 0): it takes the guarded generic path.
 #include <cfloat>
 
 #include "gact_device.cuh"
@@ -56,9 +58,11 @@ __device__ __forceinline__ void code_chunk_guarded(const QTensor& T, int64_t e, 
   store_unit_guarded<BITS>(T.packed, e, T.nwords, quantize_chunk<BITS>(v, mn, inv, r));
 }
 
-// Last tile of a tensor with G >= 256 (one short group): guarded loads, warp reduction.
+// One tile of a tensor with G >= 256, full or partial (the group may be short): guarded
+// element loads, warp reduction, per-lane division. The slow generic path, out of line.
 template <int DT, int BITS, bool STATS>
-__device__ void partial_tile_big(const QTensor& T, int64_t e0, int log2g, float Lf, int lane) {
+__device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g, float Lf,
+                                          int lane) {
   const int cpl = 1 << (log2g - 8);
   float lmn = FLT_MAX, lmx = -FLT_MAX;  // neutral; the tile has at least one element
   for (int c = 0; c < cpl; ++c) {
@@ -87,89 +91,90 @@ __device__ void partial_tile_big(const QTensor& T, int64_t e0, int log2g, float 
 }
 
 // ---------------------------------------------------------------------------------------
-// G in {256, 512, 1024}: CPL = G/256 chunks per lane kept in registers.
+// G in {256, 512, 1024}: CPL = G/256 chunks per lane, U = kQuantUnit/CPL tiles per unit,
+// all in registers.
+#ifndef GACT_Q_UNIT
+#define GACT_Q_UNIT 4
+#endif
+#ifndef GACT_Q_MINB
+#define GACT_Q_MINB 2
+#endif
+constexpr int kQuantUnit = GACT_Q_UNIT;
+static_assert(kQuantUnit <= kTileAlign && kTileAlign % kQuantUnit == 0, "unit must divide the tile alignment");
+
 template <int DT, int BITS, int CPL, int MAXB, bool STATS>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
     quantize_big_kernel(const __grid_constant__ QBatch<MAXB> P) {
-  constexpr int U = CPL == 1 ? 4 : (CPL == 2 ? 2 : 1);
-  constexpr int TE = CPL * kWarpTile;
+  constexpr int U = kQuantUnit / CPL > 0 ? kQuantUnit / CPL : 1;
+  constexpr int TE = CPL * kWarpTile;  // == G
   const int lane = threadIdx.x & 31;
   const int64_t W = (int64_t)gridDim.x * kWarps;
   const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
+  const int64_t units = P.tiles_total / U;
   int cur = 0;
-  for (int64_t base = gw; base < P.tiles_total; base += (int64_t)U * W) {
-    int tix[U];
-    int64_t e0[U];
-    bool full[U], valid[U];
+  for (int64_t u = gw; u < units; u += W) {
+    cur = advance_cursor(P, cur, u * U);
+    const QTensor& T = P.t[cur];
+    const int64_t e_base = (u * U - P.tile_start[cur]) * TE;  // first element of the unit
+    if (e_base + U * TE > T.n) {  // the tensor's last unit: guarded, one tile at a time
+      for (int k = 0; k < U; ++k)
+        if (e_base + k * TE < T.n) tile_generic<DT, BITS, STATS>(T, e_base + k * TE, P.log2g, Lf, lane);
+      continue;
+    }
+    const int64_t e_lane = e_base + lane * kChunk;
     Raw8<DT> raw[U][CPL];
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int64_t tile = base + (int64_t)k * W;
-      valid[k] = tile < P.tiles_total;
-      full[k] = false;
-      tix[k] = cur;
-      e0[k] = 0;
-      if (valid[k]) {
-        cur = advance_cursor(P, cur, tile);
-        tix[k] = cur;
-        e0[k] = (tile - P.tile_start[cur]) * TE;
-        full[k] = e0[k] + TE <= P.t[cur].n;
-        if (full[k]) {
+    for (int k = 0; k < U; ++k)
 #pragma unroll
-          for (int c = 0; c < CPL; ++c)
-            load8<DT>(raw[k][c], P.t[cur].x, e0[k] + c * kWarpTile + lane * kChunk);
-        }
-      }
+      for (int c = 0; c < CPL; ++c) load8<DT>(raw[k][c], T.x, e_lane + k * TE + c * kWarpTile);
+    uint4 rnd[U][CPL];
+    if constexpr (!STATS) {
+      const uint32_t k0 = (uint32_t)T.seed, k1 = (uint32_t)(T.seed >> 32);
+      const uint64_t blk = (uint64_t)e_lane >> 3;
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c)
+          rnd[k][c] = philox4x32_10(blk + (k * TE + c * kWarpTile) / kChunk, k0, k1);
     }
     float v[U][CPL][8];
     float mnk[U], mxk[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       float lmn = FLT_MAX, lmx = -FLT_MAX;
-      if (full[k]) {
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          widen8<DT>(raw[k][c], v[k][c]);
-          chunk_minmax(v[k][c], lmn, lmx);
-        }
+      for (int c = 0; c < CPL; ++c) {
+        widen8<DT>(raw[k][c], v[k][c]);
+        chunk_minmax(v[k][c], lmn, lmx);
       }
       mnk[k] = warp_min(lmn);
       mxk[k] = warp_max(lmx);
     }
-    // The U groups' divisions run on lanes 0..U-1 (lane l handles tile l % U).
+    // The U groups' divisions run on lanes 0..U-1 (lane l computes group l % U).
     const int sel = lane & (U - 1);
     float a = mnk[0], b = mxk[0];
 #pragma unroll
     for (int k = 1; k < U; ++k) {
-      if (sel == k) {
-        a = mnk[k];
-        b = mxk[k];
-      }
+      a = (sel == k) ? mnk[k] : a;
+      b = (sel == k) ? mxk[k] : b;
     }
     const GroupParams gp = group_params(a, b, Lf);
+    if (lane < U) {
+      const int64_t g = e_base / TE + lane;
+      T.group_min[g] = gp.mn;
+      T.group_scale[g] = gp.scale;
+    }
+    if constexpr (!STATS) {
+      unsigned char* out = reinterpret_cast<unsigned char*>(T.packed) + (e_lane * BITS) / 8;
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
-      if (full[k]) {
-        const QTensor& T = P.t[tix[k]];
+      for (int k = 0; k < U; ++k) {
         const float inv = __shfl_sync(kFull, gp.inv, k);
         const float mn = __fadd_rn(mnk[k], 0.0f);
-        if (lane == k) {
-          const int64_t g = e0[k] / TE;
-          T.group_min[g] = gp.mn;
-          T.group_scale[g] = gp.scale;
-        }
-        if constexpr (!STATS) {
-          const uint32_t k0 = (uint32_t)T.seed, k1 = (uint32_t)(T.seed >> 32);
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) {
-            const int64_t e = e0[k] + c * kWarpTile + lane * kChunk;
-            const uint4 r = philox4x32_10((uint64_t)e >> 3, k0, k1);
-            store_unit<BITS>(T.packed, e, quantize_chunk<BITS>(v[k][c], mn, inv, r));
-          }
-        }
-      } else if (valid[k]) {
-        partial_tile_big<DT, BITS, STATS>(P.t[tix[k]], e0[k], P.log2g, Lf, lane);
+        for (int c = 0; c < CPL; ++c)
+          store_unit_at<BITS>(out + ((k * TE + c * kWarpTile) * BITS) / 8,
+                              quantize_chunk<BITS>(v[k][c], mn, inv, rnd[k][c]));
       }
     }
   }
@@ -191,8 +196,9 @@ __global__ void __launch_bounds__(kThreads)
     cur = advance_cursor(P, cur, tile);
     const QTensor& T = P.t[cur];
     const int64_t e0 = (tile - P.tile_start[cur]) * TE;
+    if (e0 >= T.n) continue;  // alignment padding of the tile space
     if (e0 + TE > T.n) {
-      partial_tile_big<DT, BITS, STATS>(T, e0, P.log2g, Lf, lane);
+      tile_generic<DT, BITS, STATS>(T, e0, P.log2g, Lf, lane);
       continue;
     }
     float lmn = FLT_MAX, lmx = -FLT_MAX;
@@ -232,7 +238,43 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---------------------------------------------------------------------------------------
-// G in {32, 64, 128}: a 256-element tile holds 256/G groups of lpg = G/8 lanes each.
+// G in {32, 64, 128}: a 256-element tile holds 256/G groups of lpg = G/8 lanes each;
+// units of 4 tiles.
+template <int DT, int BITS, bool STATS>
+__device__ __forceinline__ void small_tile(const QTensor& T, int64_t e, bool full, const Raw8<DT>& raw,
+                                           uint4 rnd, int log2g, int lpg, float Lf, int lane) {
+  float v[8];
+  float lmn = FLT_MAX, lmx = -FLT_MAX;
+  if (full) {
+    widen8<DT>(raw, v);
+    chunk_minmax(v, lmn, lmx);
+  } else {
+    load8_guarded<DT>(v, T.x, e, T.n, FLT_MAX);
+    lmn = min3f(min3f(v[0], v[1], v[2]), min3f(v[3], v[4], v[5]), fminf(v[6], v[7]));
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (e + j < T.n) lmx = fmaxf(lmx, v[j]);
+  }
+  for (int o = 1; o < lpg; o <<= 1) {
+    lmn = fminf(lmn, __shfl_xor_sync(kFull, lmn, o));
+    lmx = fmaxf(lmx, __shfl_xor_sync(kFull, lmx, o));
+  }
+  const int64_t g = e >> log2g;
+  if ((g << log2g) >= T.n) return;  // group entirely beyond the tensor
+  const GroupParams gp = group_params(lmn, lmx, Lf);
+  if ((lane & (lpg - 1)) == 0) {
+    T.group_min[g] = gp.mn;
+    T.group_scale[g] = gp.scale;
+  }
+  if constexpr (!STATS) {
+    if (full) {
+      store_unit<BITS>(T.packed, e, quantize_chunk<BITS>(v, gp.mn, gp.inv, rnd));
+    } else if ((e * BITS) / 32 < T.nwords) {
+      code_chunk_guarded<DT, BITS>(T, e, gp.mn, gp.inv);
+    }
+  }
+}
+
 template <int DT, int BITS, int MAXB, bool STATS>
 __global__ void __launch_bounds__(kThreads)
     quantize_small_kernel(const __grid_constant__ QBatch<MAXB> P) {
@@ -242,64 +284,30 @@ __global__ void __launch_bounds__(kThreads)
   const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
   const int lpg = 1 << (P.log2g - 3);  // lanes per group
+  const int64_t units = P.tiles_total / U;
   int cur = 0;
-  for (int64_t base = gw; base < P.tiles_total; base += (int64_t)U * W) {
-    int tix[U];
-    int64_t e[U];
-    bool full[U], valid[U];
+  for (int64_t u = gw; u < units; u += W) {
+    cur = advance_cursor(P, cur, u * U);
+    const QTensor& T = P.t[cur];
+    const int64_t e_lane = (u * U - P.tile_start[cur]) * kWarpTile + lane * kChunk;
+    const int64_t e_warp = e_lane - lane * kChunk;
     Raw8<DT> raw[U];
+    uint4 rnd[U];
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int64_t tile = base + (int64_t)k * W;
-      valid[k] = tile < P.tiles_total;
-      full[k] = false;
-      tix[k] = cur;
-      e[k] = 0;
-      if (valid[k]) {
-        cur = advance_cursor(P, cur, tile);
-        tix[k] = cur;
-        const int64_t t0 = (tile - P.tile_start[cur]) * kWarpTile;
-        e[k] = t0 + lane * kChunk;
-        full[k] = t0 + kWarpTile <= P.t[cur].n;
-        if (full[k]) load8<DT>(raw[k], P.t[cur].x, e[k]);
-      }
+    for (int k = 0; k < U; ++k)
+      if (e_warp + (k + 1) * kWarpTile <= T.n) load8<DT>(raw[k], T.x, e_lane + k * kWarpTile);
+    if constexpr (!STATS) {
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        rnd[k] = philox4x32_10(((uint64_t)e_lane >> 3) + k * (kWarpTile / kChunk), (uint32_t)T.seed,
+                               (uint32_t)(T.seed >> 32));
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      if (!valid[k]) continue;
-      const QTensor& T = P.t[tix[k]];
-      float v[8];
-      float lmn = FLT_MAX, lmx = -FLT_MAX;
-      if (full[k]) {
-        widen8<DT>(raw[k], v);
-        chunk_minmax(v, lmn, lmx);
-      } else {
-        load8_guarded<DT>(v, T.x, e[k], T.n, FLT_MAX);
-        lmn = min3f(min3f(v[0], v[1], v[2]), min3f(v[3], v[4], v[5]), fminf(v[6], v[7]));
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (e[k] + j < T.n) lmx = fmaxf(lmx, v[j]);
-      }
-      for (int o = 1; o < lpg; o <<= 1) {
-        lmn = fminf(lmn, __shfl_xor_sync(kFull, lmn, o));
-        lmx = fmaxf(lmx, __shfl_xor_sync(kFull, lmx, o));
-      }
-      const int64_t g = e[k] >> P.log2g;
-      const int64_t g_first_elem = g << P.log2g;
-      if (g_first_elem >= T.n) continue;  // group entirely beyond the tensor
-      const GroupParams gp = group_params(lmn, lmx, Lf);
-      if ((lane & (lpg - 1)) == 0) {
-        T.group_min[g] = gp.mn;
-        T.group_scale[g] = gp.scale;
-      }
-      if constexpr (!STATS) {
-        if (full[k]) {
-          const uint4 r = philox4x32_10((uint64_t)e[k] >> 3, (uint32_t)T.seed, (uint32_t)(T.seed >> 32));
-          store_unit<BITS>(T.packed, e[k], quantize_chunk<BITS>(v, gp.mn, gp.inv, r));
-        } else if ((e[k] * BITS) / 32 < T.nwords) {
-          code_chunk_guarded<DT, BITS>(T, e[k], gp.mn, gp.inv);
-        }
-      }
+      const int64_t t0 = e_warp + k * kWarpTile;
+      if (t0 >= T.n) break;  // warp-uniform: the rest of the unit is padding
+      small_tile<DT, BITS, STATS>(T, e_lane + k * kWarpTile, t0 + kWarpTile <= T.n, raw[k], rnd[k],
+                                  P.log2g, lpg, Lf, lane);
     }
   }
 }
@@ -336,11 +344,11 @@ cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
     case 5: case 6: case 7:
       return launch_persistent<quantize_small_kernel<DT, BITS, MAXB, STATS>>(p, 4, s);
     case 8:
-      return launch_persistent<quantize_big_kernel<DT, BITS, 1, MAXB, STATS>>(p, 4, s);
+      return launch_persistent<quantize_big_kernel<DT, BITS, 1, MAXB, STATS>>(p, kQuantUnit, s);
     case 9:
-      return launch_persistent<quantize_big_kernel<DT, BITS, 2, MAXB, STATS>>(p, 2, s);
+      return launch_persistent<quantize_big_kernel<DT, BITS, 2, MAXB, STATS>>(p, kQuantUnit / 2, s);
     case 10:
-      return launch_persistent<quantize_big_kernel<DT, BITS, 4, MAXB, STATS>>(p, 1, s);
+      return launch_persistent<quantize_big_kernel<DT, BITS, 4, MAXB, STATS>>(p, kQuantUnit > 4 ? kQuantUnit / 4 : 1, s);
     default:
       return launch_persistent<quantize_twopass_kernel<DT, BITS, MAXB, STATS>>(p, 1, s);
   }

@@ -197,19 +197,20 @@ def c1_tensor(bits: int = 2, G: int = 256, n: int = 4096, seed: int = DATA_SEED)
     return x
 
 
-def exact_grid_group(G: int, bits: int, rng: np.random.Generator, e: int | None = None) -> np.ndarray:
+def exact_grid_group(G: int, bits: int, rng: np.random.Generator, e: int | None = None,
+                     e_range=(-20, 10), m_range: int = 1 << 12) -> np.ndarray:
     """G values m0 + k 2^e, k uniform in [0, 2^b - 1] with 0 and 2^b - 1 present, m0 a
-    multiple of 2^e small enough that every value is exact in binary32."""
+    multiple of 2^e (|m0| < m_range 2^e) small enough that every value is exact in binary32."""
     Lk = (1 << bits) - 1
     if e is None:
-        e = int(rng.integers(-20, 10))
+        e = int(rng.integers(*e_range))
     k = rng.integers(0, Lk + 1, size=G)
     k[rng.integers(0, G)] = 0
     j = int(rng.integers(0, G))
     while k[j] == 0 and G > 1:
         j = (j + 1) % G
     k[j] = Lk
-    m0 = int(rng.integers(-(1 << 12), 1 << 12)) * 2.0 ** e
+    m0 = int(rng.integers(-m_range, m_range)) * 2.0 ** e
     return (m0 + k.astype(np.float64) * 2.0 ** e).astype(np.float32)
 
 

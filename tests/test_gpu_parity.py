@@ -95,13 +95,15 @@ def make_input(n, dtype, seed, kind="normal"):
             if r == 1:
                 v[sl] = 3.25  # constant group
             elif r == 2:
-                v[sl] = synth.exact_grid_group(G, 2, rng)[: v[sl].size]
+                fits = dict(e_range=(-12, -2), m_range=64) if dtype == torch.float16 else {}
+                v[sl] = synth.exact_grid_group(G, 2, rng, **fits)[: v[sl].size]
             elif r == 3:
                 v[sl] = rng.integers(0, 5, v[sl].size) * 2.0 ** -149  # subnormal range
             elif r == 4:
                 v[sl] = np.where(rng.random(v[sl].size) < 0.5, -0.0, 0.0)  # signed zeros only
-            elif r == 5:
-                v[sl] = rng.standard_normal(v[sl].size) * 1e30
+            elif r == 5:  # the largest magnitudes the dtype holds without overflow
+                big = 1e4 if dtype == torch.float16 else 1e30
+                v[sl] = rng.standard_normal(v[sl].size) * big
     t = torch.from_numpy(v.astype(np.float32)).to(dtype)
     return t.cuda()
 
