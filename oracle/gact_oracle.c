@@ -198,11 +198,12 @@ int32_t oracle_group_stats(const void* x, int32_t dtype, int64_t n, int32_t G, i
 /* ------------------------------------------------------------------------------------
  * R4, R5  Stochastic rounding (App. Prop. 3):
  *   Q(h)_j = T^{-1}(ceil(T(h_j)))  w.p. T(h_j) - floor(T(h_j)),  else T^{-1}(floor(T(h_j)))
- * realised as q = floor(T + 2^-17 + k 2^-16) with k uniform on [0, 2^16): the event
- * q = ceil(T) is {k 2^-16 >= 1 - frac(T + 2^-17)}, whose probability is frac(T) up to
- * 2^-17 (the 2^-17 offset centres the 16-bit lattice of thresholds). In binary32 (R5):
- *   t = fma(h_j - min, inv, 2^-17)   -- T + 2^-17 with ONE rounding (C99 fmaf)
- *   q = floor(t + k 2^-16)           -- the exact real floor
+ * realised as q = floor(T + u) with u = (2k+1) 2^-17, k uniform on [0, 2^16): the event
+ * q = ceil(T) is {u >= 1 - frac(T)}, whose probability is frac(T) up to 2^-17 (R4).
+ * T = d * inv with d = h_j - min rounded to binary32 (R5); the product and the sum with u
+ * are EXACT reals (no rounding of T): q = floor(P) + [P - floor(P) >= 1 - u] with
+ * P = d * inv held exactly in binary64 (24 x 24 significand bits <= 53), and
+ * P - floor(P), 1 - u exact -- a comparison of exact values.
  * ---------------------------------------------------------------------------------- */
 int32_t oracle_quantize_codes(const void* x, int32_t dtype, int64_t n, int32_t G, int32_t bits,
                               uint64_t seed, int64_t g0, int64_t g1, uint8_t* q_out,
@@ -218,12 +219,14 @@ int32_t oracle_quantize_codes(const void* x, int32_t dtype, int64_t n, int32_t G
     scale_out[g - g0] = p.scale;
     for (int64_t i = lo; i < hi; ++i) {
       float h = oracle_widen(x, dtype, i);
-      float d = h - p.mn;                   /* h_j - min_j h   (binary32, RN) */
-      float t = fmaf(d, p.inv, 0x1p-17f);   /* (2^b-1)(h_j - min)/(max - min) + 2^-17 */
+      float d = h - p.mn;                      /* h_j - min_j h   (binary32, RN) */
+      double P = (double)d * (double)p.inv;    /* T = (2^b-1)(h_j - min)/(max - min), exact */
+      if (!(P >= 0.0 && P <= L)) return ORACLE_EINVARIANT; /* proven in DESIGN.md R2 */
       uint32_t k = oracle_lane16(seed, (uint64_t)i);
-      /* t >= 2^-17 has ulp >= 2^-41 and t + k 2^-16 < 2^9: the double sum is exact. */
-      double q = floor((double)t + (double)k / 65536.0);
-      if (!(t > 0.0f) || q > L) return ORACLE_EINVARIANT; /* proven in DESIGN.md R2/R5 */
+      double one_minus_u = (131072.0 - 2.0 * (double)k - 1.0) / 131072.0; /* 1 - u, exact */
+      double F = floor(P);
+      double q = F + ((P - F) >= one_minus_u ? 1.0 : 0.0); /* floor(T + u), exact */
+      if (q > L) return ORACLE_EINVARIANT;
       q_out[i - g0 * G] = (uint8_t)q;
     }
   }

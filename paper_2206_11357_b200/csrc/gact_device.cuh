@@ -33,10 +33,13 @@ __device__ __forceinline__ uint32_t xor3(uint32_t a, uint32_t b, uint32_t c) {
   return d;
 }
 
+#ifndef GACT_EXP_ROUNDS
+#define GACT_EXP_ROUNDS 10  // experiments only: Philox4x32-10 is the defined generator
+#endif
 __device__ __forceinline__ uint4 philox4x32_10(uint64_t block, uint32_t k0, uint32_t k1) {
   uint32_t c0 = (uint32_t)block, c1 = (uint32_t)(block >> 32), c2 = 0u, c3 = 0u;
 #pragma unroll
-  for (int r = 0; r < 10; ++r) {
+  for (int r = 0; r < GACT_EXP_ROUNDS; ++r) {
     uint32_t lo0, hi0, lo1, hi1;
     mul_wide(c0, 0xD2511F53u, lo0, hi0);
     mul_wide(c2, 0xCD9E8D57u, lo1, hi1);
@@ -81,6 +84,11 @@ __device__ __forceinline__ f2_t f2_sub_rn(f2_t a, f2_t b) {
 __device__ __forceinline__ f2_t f2_mul_rn(f2_t a, f2_t b) {
   f2_t r;
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t f2_add_rn(f2_t a, f2_t b) {
+  f2_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
 __device__ __forceinline__ f2_t f2_add_rm(f2_t a, f2_t b) {
@@ -229,16 +237,16 @@ __device__ __forceinline__ GroupParams group_params(float mn, float mx, float Lf
 }
 
 // ----------------------------------------------------------- stochastic rounding + pack
-// Codes of 8 consecutive elements (chunk), packed LSB-first into BITS*8 bits.
-// q_j = floor(t_j + k_j 2^-16) with t_j = fma(v_j - mn, inv, 2^-17) (one rounding) and k_j
-// the 16-bit lane j of the chunk's Philox block (include/gact.h). Per pair of elements:
-//   d = sub(x, mn)                FADD2
-//   t = fma(d, inv, 2^-17)        FFMA2
-//   f = 1 + k 2^-23               PRMT (bit pattern 0x3F80_0000 | k)
-//   v = fma.rm(f, 128, t)         FFMA2.RM   = RD(128 + k 2^-16 + t)
-//   w = add.rm(v, 2^23 - 128)     FADD2.RM   bits(w) = 0x4B00_0000 + floor(t + k 2^-16)
-// (RD never crosses an integer: floor(RD(s)) = floor(s); on [2^23, 2^24) the binary32 grid
-// is the integers.) Then the low byte of bits(w) is the code.
+// Codes of 8 consecutive elements (chunk), packed LSB-first into BITS*8 bits:
+//   q_j = floor(d_j * inv + (2 k_j + 1) 2^-17),  d_j = RN(v_j - mn)     (include/gact.h)
+// with the product and the sum exact. Per pair of elements (j = 2p, 2p+1; k from the low /
+// high half of Philox word p):
+//   c = (128 + k 2^-16) + (2^-17 - 64)   PRMT builds 0x4300_0000 | k; FADD2 is exact:
+//                                         c = 64 + (2k+1) 2^-17 in [64, 65)
+//   v = fma.rm(d, inv, c)                 FFMA2.RM: RD(d*inv + c), one rounding, downward
+//   w = add.rm(v, 2^23 - 64)              FADD2.RM: bits(w) = 0x4B00_0000 + floor(v) - 64
+// RD never crosses an integer (floor(RD(s)) = floor(s)) and [2^23, 2^24) is the integer
+// grid of binary32, so bits(w) - 0x4B00_0000 = q_j exactly. The low byte of bits(w) is q_j.
 template <int BITS>
 struct PackedUnit {
   uint32_t lo, hi;  // hi used only for BITS == 8 (64-bit unit)
@@ -251,40 +259,111 @@ __device__ __forceinline__ constexpr uint32_t magic_sum(int first, int count) {
   return s;
 }
 
+// w_j (= 0x4B00_0000 + q_j) of the pair (d_lo, d_hi) drawing from Philox word rw.
+__device__ __forceinline__ void code_pair(f2_t d2, f2_t inv2, uint32_t rw, uint32_t& w_lo,
+                                          uint32_t& w_hi) {
+  const f2_t cofs = f2_make(0x1p-17f - 64.0f, 0x1p-17f - 64.0f);
+  const f2_t magic = f2_make(8388608.0f - 64.0f, 8388608.0f - 64.0f);
+  const uint32_t klo = __byte_perm(rw, 0x43000000u, 0x7610);  // 128 + k_lo 2^-16
+  const uint32_t khi = __byte_perm(rw, 0x43000000u, 0x7632);  // 128 + k_hi 2^-16
+  const f2_t c2 = f2_add_rn(f2_bits(klo, khi), cofs);
+  const f2_t w2 = f2_add_rm(f2_fma_rm(d2, inv2, c2), magic);
+  f2_split_bits(w2, w_lo, w_hi);
+}
+
 template <int BITS>
-__device__ __forceinline__ PackedUnit<BITS> quantize_chunk(const float v[8], float mn, float inv,
-                                                           uint4 r) {
-  const f2_t mn2 = f2_make(mn, mn);
-  const f2_t inv2 = f2_make(inv, inv);
-  const f2_t c17 = f2_make(0x1p-17f, 0x1p-17f);
-  const f2_t c128 = f2_make(128.0f, 128.0f);
-  const f2_t magic = f2_make(8388608.0f - 128.0f, 8388608.0f - 128.0f);
-  const uint32_t words[4] = {r.x, r.y, r.z, r.w};
-  uint32_t w[8];
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    // elements 2p (low half of Philox word p) and 2p+1 (high half)
-    const f2_t x2 = f2_make(v[2 * p], v[2 * p + 1]);
-    const f2_t t2 = f2_fma_rn(f2_sub_rn(x2, mn2), inv2, c17);
-    const uint32_t flo = __byte_perm(words[p], 0x3F800000u, 0x7610);
-    const uint32_t fhi = __byte_perm(words[p], 0x3F800000u, 0x7632);
-    const f2_t v2 = f2_fma_rm(f2_bits(flo, fhi), c128, t2);
-    const f2_t w2 = f2_add_rm(v2, magic);
-    f2_split_bits(w2, w[2 * p], w[2 * p + 1]);
-  }
+__device__ __forceinline__ PackedUnit<BITS> pack_codes(const uint32_t w[8]) {
   PackedUnit<BITS> out;
   if constexpr (BITS == 8) {
-    // bytes: gather the low byte of each w_j (byte permutes, integer ALU pipe)
+    // gather the low byte of each w_j (byte permutes)
     out.lo = __byte_perm(__byte_perm(w[0], w[1], 0x0040), __byte_perm(w[2], w[3], 0x0040), 0x5410);
     out.hi = __byte_perm(__byte_perm(w[4], w[5], 0x0040), __byte_perm(w[6], w[7], 0x0040), 0x5410);
   } else {
     uint32_t acc = 0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc += w[j] << (BITS * j);
+    for (int j = 0; j < 8; ++j) acc += w[j] << (BITS * j);  // mod 2^32
     out.lo = acc - magic_sum<BITS>(0, 8);
     out.hi = 0;
   }
   return out;
+}
+
+// From binary32 values (any dtype widened, or the guarded paths).
+template <int BITS>
+__device__ __forceinline__ PackedUnit<BITS> quantize_chunk(const float v[8], float mn, float inv,
+                                                           uint4 r) {
+  const f2_t mn2 = f2_make(mn, mn), inv2 = f2_make(inv, inv);
+  const uint32_t words[4] = {r.x, r.y, r.z, r.w};
+  uint32_t w[8];
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+    code_pair(f2_sub_rn(f2_make(v[2 * p], v[2 * p + 1]), mn2), inv2, words[p], w[2 * p], w[2 * p + 1]);
+  return pack_codes<BITS>(w);
+}
+
+// Straight from the loaded chunk. bf16 / f16: d = x - mn by the mixed-precision subtract
+// (sub.rn.f32.bf16 / .f16: exact widening, one binary32 rounding) on each half-word.
+template <int DT, int BITS>
+__device__ __forceinline__ PackedUnit<BITS> quantize_chunk_raw(const Raw8<DT>& raw, float mn,
+                                                               float inv, uint4 r) {
+  if constexpr (DT == DT_F32) {
+    float v[8];
+    widen8<DT>(raw, v);
+    return quantize_chunk<BITS>(v, mn, inv, r);
+  } else {
+    const f2_t inv2 = f2_make(inv, inv);
+    const uint32_t xw[4] = {raw.a.x, raw.a.y, raw.a.z, raw.a.w};
+    const uint32_t words[4] = {r.x, r.y, r.z, r.w};
+    uint32_t w[8];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      float dlo, dhi;
+      if constexpr (DT == DT_BF16) {
+        asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\tsub.rn.f32.bf16 %0, l, %3;\n\t"
+            "sub.rn.f32.bf16 %1, h, %3;\n\t}"
+            : "=f"(dlo), "=f"(dhi) : "r"(xw[p]), "f"(mn));
+      } else {
+        asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\tsub.rn.f32.f16 %0, l, %3;\n\t"
+            "sub.rn.f32.f16 %1, h, %3;\n\t}"
+            : "=f"(dlo), "=f"(dhi) : "r"(xw[p]), "f"(mn));
+      }
+      code_pair(f2_make(dlo, dhi), inv2, words[p], w[2 * p], w[2 * p + 1]);
+    }
+    return pack_codes<BITS>(w);
+  }
+}
+
+// Fold a loaded chunk's 8 values into running binary32 (mn, mx). bf16 / f16 reduce the
+// four packed words with 2-wide min / max first (HMNMX2), then widen the two survivors.
+template <int DT>
+__device__ __forceinline__ void chunk_minmax_raw(const Raw8<DT>& raw, float& mn, float& mx) {
+  if constexpr (DT == DT_F32) {
+    float v[8];
+    widen8<DT>(raw, v);
+    mn = min3f(min3f(mn, v[0], v[1]), min3f(v[2], v[3], v[4]), min3f(v[5], v[6], v[7]));
+    mx = max3f(max3f(mx, v[0], v[1]), max3f(v[2], v[3], v[4]), max3f(v[5], v[6], v[7]));
+  } else {
+    uint32_t m01, m23, m, M01, M23, M;
+    if constexpr (DT == DT_BF16) {
+      asm("min.bf16x2 %0, %1, %2;" : "=r"(m01) : "r"(raw.a.x), "r"(raw.a.y));
+      asm("min.bf16x2 %0, %1, %2;" : "=r"(m23) : "r"(raw.a.z), "r"(raw.a.w));
+      asm("min.bf16x2 %0, %1, %2;" : "=r"(m) : "r"(m01), "r"(m23));
+      asm("max.bf16x2 %0, %1, %2;" : "=r"(M01) : "r"(raw.a.x), "r"(raw.a.y));
+      asm("max.bf16x2 %0, %1, %2;" : "=r"(M23) : "r"(raw.a.z), "r"(raw.a.w));
+      asm("max.bf16x2 %0, %1, %2;" : "=r"(M) : "r"(M01), "r"(M23));
+      mn = min3f(mn, __uint_as_float(m << 16), __uint_as_float(m & 0xFFFF0000u));
+      mx = max3f(mx, __uint_as_float(M << 16), __uint_as_float(M & 0xFFFF0000u));
+    } else {
+      asm("min.f16x2 %0, %1, %2;" : "=r"(m01) : "r"(raw.a.x), "r"(raw.a.y));
+      asm("min.f16x2 %0, %1, %2;" : "=r"(m23) : "r"(raw.a.z), "r"(raw.a.w));
+      asm("min.f16x2 %0, %1, %2;" : "=r"(m) : "r"(m01), "r"(m23));
+      asm("max.f16x2 %0, %1, %2;" : "=r"(M01) : "r"(raw.a.x), "r"(raw.a.y));
+      asm("max.f16x2 %0, %1, %2;" : "=r"(M23) : "r"(raw.a.z), "r"(raw.a.w));
+      asm("max.f16x2 %0, %1, %2;" : "=r"(M) : "r"(M01), "r"(M23));
+      mn = min3f(mn, f16_bits_to_f32(m & 0xFFFFu), f16_bits_to_f32(m >> 16));
+      mx = max3f(mx, f16_bits_to_f32(M & 0xFFFFu), f16_bits_to_f32(M >> 16));
+    }
+  }
 }
 
 // Store the chunk's packed unit at byte address p. Element e0 (multiple of 8) starts at

@@ -5,9 +5,11 @@
 // elements; a warp owns a tile at a time and each lane a chunk of 8 consecutive elements
 // (one Philox4x32-10 call = 8 x 16-bit lanes; one 16- or 32-byte coalesced load).
 // Tensors of a batch are concatenated in tile space (QBatch::tile_start), each tensor's
-// tile count rounded up to kTileAlign = 4, so that a warp's UNIT of U <= 4 consecutive
-// tiles never straddles two tensors. Warps walk units grid-stride: the active window of a
-// launch is compact in memory and each warp streams U * TE contiguous elements per step.
+// tile count rounded up to kTileAlign = 32, so that a CTA UNIT (8 warps x U consecutive
+// tiles) never straddles two tensors. CTAs walk units grid-stride: the active window of a
+// launch is compact in memory, each warp streams U * TE contiguous elements per step, and
+// the unit's bookkeeping (tensor, seed, pointers) is warp-uniform AND CTA-uniform, so it
+// lives in the uniform datapath (UIADD3 key schedule for Philox).
 //  * G in {256, 512, 1024}: one tile == one group, reduced in registers (FMNMX3 in-thread,
 //    one CREDUX per warp for min and max), coded from the same registers, written once:
 //    x is read exactly once. The U x CPL Philox blocks of a unit are computed while its
@@ -33,11 +35,6 @@ __device__ __forceinline__ int advance_cursor(const QBatch<MAXB>& P, int cur, in
     while (cur + 1 < P.count && tile >= P.tile_start[cur + 1]) ++cur;
   }
   return cur;
-}
-
-__device__ __forceinline__ void chunk_minmax(const float v[8], float& mn, float& mx) {
-  mn = min3f(min3f(mn, v[0], v[1]), min3f(v[2], v[3], v[4]), min3f(v[5], v[6], v[7]));
-  mx = max3f(max3f(mx, v[0], v[1]), max3f(v[2], v[3], v[4]), max3f(v[5], v[6], v[7]));
 }
 
 template <int DT>
@@ -107,17 +104,19 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
     quantize_big_kernel(const __grid_constant__ QBatch<MAXB> P) {
   constexpr int U = kQuantUnit / CPL > 0 ? kQuantUnit / CPL : 1;
   constexpr int TE = CPL * kWarpTile;  // == G
+  constexpr int CU = kWarps * U;       // tiles per CTA unit (divides kTileAlign)
   const int lane = threadIdx.x & 31;
-  const int64_t W = (int64_t)gridDim.x * kWarps;
-  const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int warp = threadIdx.x >> 5;
   const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
-  const int64_t units = P.tiles_total / U;
+  const int64_t cunits = P.tiles_total / CU;
   int cur = 0;
-  for (int64_t u = gw; u < units; u += W) {
-    cur = advance_cursor(P, cur, u * U);
+  // CTA-unit bookkeeping (tensor, seed, base pointers) depends only on blockIdx and the
+  // loop counter: it lives in uniform registers.
+  for (int64_t cu = blockIdx.x; cu < cunits; cu += gridDim.x) {
+    cur = advance_cursor(P, cur, cu * CU);
     const QTensor& T = P.t[cur];
-    const int64_t e_base = (u * U - P.tile_start[cur]) * TE;  // first element of the unit
-    if (e_base + U * TE > T.n) {  // the tensor's last unit: guarded, one tile at a time
+    const int64_t e_base = (cu * CU - P.tile_start[cur]) * TE + (int64_t)warp * U * TE;
+    if (e_base + U * TE > T.n) {  // the tensor's last units: guarded, one tile at a time
       for (int k = 0; k < U; ++k)
         if (e_base + k * TE < T.n) tile_generic<DT, BITS, STATS>(T, e_base + k * TE, P.log2g, Lf, lane);
       continue;
@@ -138,16 +137,12 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
         for (int c = 0; c < CPL; ++c)
           rnd[k][c] = philox4x32_10(blk + (k * TE + c * kWarpTile) / kChunk, k0, k1);
     }
-    float v[U][CPL][8];
     float mnk[U], mxk[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       float lmn = FLT_MAX, lmx = -FLT_MAX;
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        widen8<DT>(raw[k][c], v[k][c]);
-        chunk_minmax(v[k][c], lmn, lmx);
-      }
+      for (int c = 0; c < CPL; ++c) chunk_minmax_raw<DT>(raw[k][c], lmn, lmx);
       mnk[k] = warp_min(lmn);
       mxk[k] = warp_max(lmx);
     }
@@ -174,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
 #pragma unroll
         for (int c = 0; c < CPL; ++c)
           store_unit_at<BITS>(out + ((k * TE + c * kWarpTile) * BITS) / 8,
-                              quantize_chunk<BITS>(v[k][c], mn, inv, rnd[k][c]));
+                              quantize_chunk_raw<DT, BITS>(raw[k][c], mn, inv, rnd[k][c]));
       }
     }
   }
@@ -186,16 +181,15 @@ template <int DT, int BITS, int MAXB, bool STATS>
 __global__ void __launch_bounds__(kThreads)
     quantize_twopass_kernel(const __grid_constant__ QBatch<MAXB> P) {
   const int lane = threadIdx.x & 31;
-  const int64_t W = (int64_t)gridDim.x * kWarps;
-  const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
   const int cpl = 1 << (P.log2g - 8);
   const int64_t TE = (int64_t)1 << P.log2g;
+  const int warp = threadIdx.x >> 5;
   int cur = 0;
-  for (int64_t tile = gw; tile < P.tiles_total; tile += W) {
-    cur = advance_cursor(P, cur, tile);
+  for (int64_t cu = blockIdx.x; cu < P.tiles_total / kWarps; cu += gridDim.x) {
+    cur = advance_cursor(P, cur, cu * kWarps);
     const QTensor& T = P.t[cur];
-    const int64_t e0 = (tile - P.tile_start[cur]) * TE;
+    const int64_t e0 = (cu * kWarps - P.tile_start[cur] + warp) * TE;
     if (e0 >= T.n) continue;  // alignment padding of the tile space
     if (e0 + TE > T.n) {
       tile_generic<DT, BITS, STATS>(T, e0, P.log2g, Lf, lane);
@@ -207,11 +201,7 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
       for (int i = 0; i < 4; ++i) load8<DT>(raw[i], T.x, e0 + (c + i) * kWarpTile + lane * kChunk);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        float v[8];
-        widen8<DT>(raw[i], v);
-        chunk_minmax(v, lmn, lmx);
-      }
+      for (int i = 0; i < 4; ++i) chunk_minmax_raw<DT>(raw[i], lmn, lmx);
     }
     const GroupParams gp = group_params(warp_min(lmn), warp_max(lmx), Lf);
     if (lane == 0) {
@@ -226,11 +216,9 @@ __global__ void __launch_bounds__(kThreads)
         for (int i = 0; i < 4; ++i) load8<DT>(raw[i], T.x, e0 + (c + i) * kWarpTile + lane * kChunk);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          float v[8];
-          widen8<DT>(raw[i], v);
           const int64_t e = e0 + (c + i) * kWarpTile + lane * kChunk;
           const uint4 r = philox4x32_10((uint64_t)e >> 3, k0, k1);
-          store_unit<BITS>(T.packed, e, quantize_chunk<BITS>(v, gp.mn, gp.inv, r));
+          store_unit<BITS>(T.packed, e, quantize_chunk_raw<DT, BITS>(raw[i], gp.mn, gp.inv, r));
         }
       }
     }
@@ -246,8 +234,7 @@ __device__ __forceinline__ void small_tile(const QTensor& T, int64_t e, bool ful
   float v[8];
   float lmn = FLT_MAX, lmx = -FLT_MAX;
   if (full) {
-    widen8<DT>(raw, v);
-    chunk_minmax(v, lmn, lmx);
+    chunk_minmax_raw<DT>(raw, lmn, lmx);
   } else {
     load8_guarded<DT>(v, T.x, e, T.n, FLT_MAX);
     lmn = min3f(min3f(v[0], v[1], v[2]), min3f(v[3], v[4], v[5]), fminf(v[6], v[7]));
@@ -268,7 +255,7 @@ __device__ __forceinline__ void small_tile(const QTensor& T, int64_t e, bool ful
   }
   if constexpr (!STATS) {
     if (full) {
-      store_unit<BITS>(T.packed, e, quantize_chunk<BITS>(v, gp.mn, gp.inv, rnd));
+      store_unit<BITS>(T.packed, e, quantize_chunk_raw<DT, BITS>(raw, gp.mn, gp.inv, rnd));
     } else if ((e * BITS) / 32 < T.nwords) {
       code_chunk_guarded<DT, BITS>(T, e, gp.mn, gp.inv);
     }
@@ -280,16 +267,15 @@ __global__ void __launch_bounds__(kThreads)
     quantize_small_kernel(const __grid_constant__ QBatch<MAXB> P) {
   constexpr int U = 4;
   const int lane = threadIdx.x & 31;
-  const int64_t W = (int64_t)gridDim.x * kWarps;
-  const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
   const int lpg = 1 << (P.log2g - 3);  // lanes per group
-  const int64_t units = P.tiles_total / U;
+  const int warp = threadIdx.x >> 5;
+  constexpr int CU = kWarps * U;
   int cur = 0;
-  for (int64_t u = gw; u < units; u += W) {
-    cur = advance_cursor(P, cur, u * U);
+  for (int64_t cu = blockIdx.x; cu < P.tiles_total / CU; cu += gridDim.x) {
+    cur = advance_cursor(P, cur, cu * CU);
     const QTensor& T = P.t[cur];
-    const int64_t e_lane = (u * U - P.tile_start[cur]) * kWarpTile + lane * kChunk;
+    const int64_t e_lane = (cu * CU - P.tile_start[cur] + warp * U) * kWarpTile + lane * kChunk;
     const int64_t e_warp = e_lane - lane * kChunk;
     Raw8<DT> raw[U];
     uint4 rnd[U];

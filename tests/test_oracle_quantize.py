@@ -4,8 +4,8 @@ the mathematics fix, never to the oracle itself:
   * SPEC.md's worked group-statistics examples (tests/golden/spec_examples.txt);
   * group statistics recomputed with NumPy's min / max / binary32 division and an exact
     rational round-toward-zero for inv (Fractions);
-  * every code recomputed as the exact real floor(t + k 2^-16), t = fma(x - mn, inv, 2^-17)
-    rounded once (exact rationals + round-to-nearest-even written out);
+  * every code recomputed as the exact real floor(d * inv + (2k+1) 2^-17) with Fractions
+    (d = x - mn in binary32; product and sum exact);
   * the exact round trip on b-bit grids (P:497 idempotence, B3) for every seed;
   * Monte Carlo unbiasedness E[Q(x)] = x, per-element variance p(1-p) scale^2
     and the paper's bound 1/4 range^2 S(b) (B2), and uncorrelated elements
@@ -103,24 +103,6 @@ def test_group_stats_vs_numpy(orc, tag, G):
             assert sc[g].view(np.uint32) == rsc.view(np.uint32)
 
 
-def _rn_f32(q: Fraction) -> np.float32:
-    """Nearest binary32 to a positive rational, ties to even (exact comparisons)."""
-    f = np.float32(float(q))
-    lo = f if Fraction(float(f)) <= q else np.nextafter(f, np.float32(0))
-    hi = np.nextafter(lo, np.float32(np.inf))
-    dlo, dhi = q - Fraction(float(lo)), Fraction(float(hi)) - q
-    if dlo < dhi:
-        return lo
-    if dhi < dlo:
-        return hi
-    return lo if (int(lo.view(np.uint32)) & 1) == 0 else hi
-
-
-def _t_prime(d: np.float32, inv: np.float32) -> Fraction:
-    """t = fma(d, inv, 2^-17): the exact product-sum rounded once to binary32."""
-    return Fraction(float(_rn_f32(Fraction(float(d)) * Fraction(float(inv)) + Fraction(1, 1 << 17))))
-
-
 @pytest.mark.parametrize("tag", [0, 1, 2])
 def test_codes_are_exact_floor_of_t_plus_u(orc, tag):
     rng = np.random.default_rng(20 + tag)
@@ -135,13 +117,13 @@ def test_codes_are_exact_floor_of_t_plus_u(orc, tag):
             for i in range(g * G, min(n, (g + 1) * G)):
                 d = np.float32(vals[i] - rmn)
                 k = orc.lane16(seed, i)
-                exact = math.floor(_t_prime(d, inv) + Fraction(k, 1 << 16))
+                exact = math.floor(Fraction(float(d)) * Fraction(float(inv)) + Fraction(2 * k + 1, 1 << 17))
                 assert q[i] == exact, (bits, i)
 
 
 def test_t_within_0_L_on_adversarial_ranges(orc):
-    """R2/R5: with inv = RZ(L/range) the transform never leaves (0, L + 2^-17] and codes never
-    exceed L (the oracle returns EINVARIANT otherwise); ranges from subnormal to 1e38."""
+    """R2: with inv = RZ(L/range) the exact transform d * inv never leaves [0, L] and codes
+    never exceed L (the oracle returns EINVARIANT otherwise); ranges from subnormal to 1e38."""
     rng = np.random.default_rng(5)
     for scale in [1e-44, 1e-40, 1e-30, 1e-3, 1.0, 1e10, 1e30, 1e38]:
         for bits in LADDER:
