@@ -43,15 +43,29 @@ __device__ __forceinline__ uint2 load_unit(const uint32_t* packed, int64_t e0, i
   }
 }
 
-// Bit pattern 0x4B00_0000 | q_j (the float 2^23 + q_j) of element j of the unit.
+// The 8 bit patterns 0x4B00_0000 | q_j (the floats 2^23 + q_j) of a chunk's unit.
+//   b = 8: one byte permute per element (PRMT with the 0x4B byte);
+//   b = 4: even / odd nibbles split into bytes with two masks, then byte permutes;
+//   b = 1, 2: shift + mask-or per element.
 template <int BITS>
-__device__ __forceinline__ uint32_t magic_code(uint2 u, int j) {
+__device__ __forceinline__ void magic_codes(uint2 u, uint32_t m[8]) {
   if constexpr (BITS == 8) {
-    const uint32_t w = j < 4 ? u.x : u.y;
-    // bytes: [q, 0x00, 0x00, 0x4B]
-    return __byte_perm(w, 0x4B000000u, 0x7540 | (j & 3));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      m[j] = __byte_perm(u.x, 0x4B000000u, 0x7540 | j);
+      m[4 + j] = __byte_perm(u.y, 0x4B000000u, 0x7540 | j);
+    }
+  } else if constexpr (BITS == 4) {
+    const uint32_t ev = u.x & 0x0F0F0F0Fu;         // bytes: q0 q2 q4 q6
+    const uint32_t od = (u.x >> 4) & 0x0F0F0F0Fu;  // bytes: q1 q3 q5 q7
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      m[2 * j] = __byte_perm(ev, 0x4B000000u, 0x7540 | j);
+      m[2 * j + 1] = __byte_perm(od, 0x4B000000u, 0x7540 | j);
+    }
   } else {
-    return ((u.x >> (j * BITS)) & ((1u << BITS) - 1u)) | 0x4B000000u;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) m[j] = ((u.x >> (j * BITS)) & ((1u << BITS) - 1u)) | 0x4B000000u;
   }
 }
 
@@ -60,10 +74,11 @@ template <int BITS>
 __device__ __forceinline__ void decode8(uint2 u, float mn, float scale, float y[8]) {
   const f2_t mn2 = f2_make(mn, mn), sc2 = f2_make(scale, scale);
   const f2_t magic = f2_make(8388608.0f, 8388608.0f);
+  uint32_t m[8];
+  magic_codes<BITS>(u, m);
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
-    const f2_t w2 = f2_bits(magic_code<BITS>(u, 2 * p), magic_code<BITS>(u, 2 * p + 1));
-    const f2_t q2 = f2_sub_rn(w2, magic);  // exact: q_j as float
+    const f2_t q2 = f2_sub_rn(f2_bits(m[2 * p], m[2 * p + 1]), magic);  // exact: q_j as float
     f2_split(f2_fma_rn(q2, sc2, mn2), y[2 * p], y[2 * p + 1]);
   }
 }
@@ -102,61 +117,73 @@ __device__ __forceinline__ void store1(void* ybase, int64_t e, float y) {
   }
 }
 
+// The tail of a tensor (its last, partial unit): chunk by chunk, guarded. Out of line.
+template <int DT, int BITS>
+__device__ __noinline__ void dequant_generic(const DTensor T, int64_t e_first, int chunks,
+                                             int log2g, int lane) {
+  for (int k = 0; k < chunks; ++k) {
+    const int64_t e = e_first + (int64_t)k * kDequantTileElems + lane * kChunk;
+    if (e >= T.n) continue;
+    const uint2 unit = load_unit<BITS>(T.packed, e, T.n);
+    float y[8];
+    decode8<BITS>(unit, __ldg(T.group_min + (e >> log2g)), __ldg(T.group_scale + (e >> log2g)), y);
+    if (e + kChunk <= T.n) {
+      store8<DT>(T.y, e, y);
+    } else {
+      for (int j = 0; j < 8; ++j)
+        if (e + j < T.n) store1<DT>(T.y, e + j, y[j]);
+    }
+  }
+}
+
 #ifndef GACT_D_UNIT
 #define GACT_D_UNIT 4
 #endif
 #ifndef GACT_D_MINB
 #define GACT_D_MINB 1
 #endif
-constexpr int kDequantUnit = GACT_D_UNIT;
+constexpr int kDequantUnit = GACT_D_UNIT;  // tiles per warp per unit
+static_assert(kDequantAlign % (kWarps * kDequantUnit) == 0, "CTA unit must divide the alignment");
 
+// CTAs walk units of 8 warps x U tiles (tensors padded to kDequantAlign tiles), so the
+// unit's tensor bookkeeping is CTA-uniform; a warp decodes U consecutive tiles.
 template <int DT, int BITS, int MAXB>
 __global__ void __launch_bounds__(kThreads, GACT_D_MINB)
     dequantize_kernel(const __grid_constant__ DBatch<MAXB> P) {
   constexpr int U = kDequantUnit;
+  constexpr int CU = kWarps * U;
+  constexpr int TE = (int)kDequantTileElems;
   const int lane = threadIdx.x & 31;
-  const int64_t W = (int64_t)gridDim.x * kWarps;
-  const int64_t gw = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int warp = threadIdx.x >> 5;
   int cur = 0;
-  for (int64_t base = gw; base < P.tiles_total; base += (int64_t)U * W) {
-    int tix[U];
-    int64_t e[U];
-    bool valid[U];
+  for (int64_t cu = blockIdx.x; cu < P.tiles_total / CU; cu += gridDim.x) {
+    cur = advance_cursor(P, cur, cu * CU);
+    const DTensor& T = P.t[cur];
+    const int64_t e_base = (cu * CU - P.tile_start[cur] + (int64_t)warp * U) * TE;
+    if (e_base + U * TE > T.n) {
+      if (e_base < T.n) dequant_generic<DT, BITS>(T, e_base, U, P.log2g, lane);
+      continue;
+    }
+    const int64_t e_lane = e_base + lane * kChunk;
+    const unsigned char* src = reinterpret_cast<const unsigned char*>(T.packed) + (e_lane * BITS) / 8;
     uint2 unit[U];
     float mn[U], sc[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      const int64_t tile = base + (int64_t)k * W;
-      valid[k] = tile < P.tiles_total;
-      tix[k] = cur;
-      e[k] = 0;
-      if (valid[k]) {
-        cur = advance_cursor(P, cur, tile);
-        tix[k] = cur;
-        const DTensor& T = P.t[cur];
-        e[k] = (tile - P.tile_start[cur]) * kDequantTileElems + lane * kChunk;
-        valid[k] = e[k] < T.n;  // lanes past the end of a partial tile idle
-        if (valid[k]) {
-          unit[k] = load_unit<BITS>(T.packed, e[k], T.n);
-          const int64_t g = e[k] >> P.log2g;
-          mn[k] = __ldg(T.group_min + g);
-          sc[k] = __ldg(T.group_scale + g);
-        }
-      }
+      const unsigned char* p = src + (k * TE * BITS) / 8;
+      if constexpr (BITS == 1) unit[k] = make_uint2(__ldg(p), 0u);
+      else if constexpr (BITS == 2) unit[k] = make_uint2(__ldg(reinterpret_cast<const uint16_t*>(p)), 0u);
+      else if constexpr (BITS == 4) unit[k] = make_uint2(__ldg(reinterpret_cast<const uint32_t*>(p)), 0u);
+      else unit[k] = __ldg(reinterpret_cast<const uint2*>(p));
+      const int64_t g = (e_lane + k * TE) >> P.log2g;
+      mn[k] = __ldg(T.group_min + g);
+      sc[k] = __ldg(T.group_scale + g);
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      if (!valid[k]) continue;
-      const DTensor& T = P.t[tix[k]];
       float y[8];
       decode8<BITS>(unit[k], mn[k], sc[k], y);
-      if (e[k] + kChunk <= T.n) {
-        store8<DT>(T.y, e[k], y);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (e[k] + j < T.n) store1<DT>(T.y, e[k] + j, y[j]);
-      }
+      store8<DT>(T.y, e_lane + k * TE, y);
     }
   }
 }
@@ -175,7 +202,7 @@ cudaError_t launch_d(const DBatch<MAXB>& p, cudaStream_t s) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t want = (p.tiles_total + kWarps * kDequantUnit - 1) / (kWarps * kDequantUnit);
+  const int64_t want = p.tiles_total / (kWarps * kDequantUnit);
   const int64_t cap = (int64_t)sms * per_sm;
   const int grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
   kernel<<<grid, kThreads, 0, s>>>(p);

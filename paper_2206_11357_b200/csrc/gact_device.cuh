@@ -260,6 +260,9 @@ __device__ __forceinline__ constexpr uint32_t magic_sum(int first, int count) {
 }
 
 // w_j (= 0x4B00_0000 + q_j) of the pair (d_lo, d_hi) drawing from Philox word rw.
+// c = 64 + (2k+1) 2^-17: PRMT builds 0x4300_0000 | k = 128 + k 2^-16, then one exact FADD2
+// adds 2^-17 - 64. (Building c in the integer pipe instead -- funnel shift + lop3 -- was
+// measured slower: it overloads the ALU pipe that the Philox xors and byte permutes use.)
 __device__ __forceinline__ void code_pair(f2_t d2, f2_t inv2, uint32_t rw, uint32_t& w_lo,
                                           uint32_t& w_hi) {
   const f2_t cofs = f2_make(0x1p-17f - 64.0f, 0x1p-17f - 64.0f);
@@ -351,8 +354,8 @@ __device__ __forceinline__ void chunk_minmax_raw(const Raw8<DT>& raw, float& mn,
       asm("max.bf16x2 %0, %1, %2;" : "=r"(M01) : "r"(raw.a.x), "r"(raw.a.y));
       asm("max.bf16x2 %0, %1, %2;" : "=r"(M23) : "r"(raw.a.z), "r"(raw.a.w));
       asm("max.bf16x2 %0, %1, %2;" : "=r"(M) : "r"(M01), "r"(M23));
-      mn = min3f(mn, __uint_as_float(m << 16), __uint_as_float(m & 0xFFFF0000u));
-      mx = max3f(mx, __uint_as_float(M << 16), __uint_as_float(M & 0xFFFF0000u));
+      mn = min3f(mn, __uint_as_float(__byte_perm(m, 0u, 0x1044)), __uint_as_float(m & 0xFFFF0000u));
+      mx = max3f(mx, __uint_as_float(__byte_perm(M, 0u, 0x1044)), __uint_as_float(M & 0xFFFF0000u));
     } else {
       asm("min.f16x2 %0, %1, %2;" : "=r"(m01) : "r"(raw.a.x), "r"(raw.a.y));
       asm("min.f16x2 %0, %1, %2;" : "=r"(m23) : "r"(raw.a.z), "r"(raw.a.w));

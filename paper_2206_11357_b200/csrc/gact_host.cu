@@ -181,7 +181,7 @@ gact_status gact_unpack_dequantize(const uint32_t* packed, const float* group_mi
   p.log2g = l2;
   p.t[0] = make_d(y, n, packed, group_min, group_scale);
   p.tile_start[0] = 0;
-  p.tiles_total = p.tile_start[1] = ceil_div(n, gact::kDequantTileElems);
+  p.tiles_total = p.tile_start[1] = gact::dequant_tiles(n);
   return from_cuda(gact::launch_dequantize<1>(p, y_dtype, bits, static_cast<cudaStream_t>(stream)));
 }
 
@@ -248,7 +248,7 @@ gact_status gact_unpack_dequantize_batch(const gact_tensor_desc* descs, int32_t 
         if (d.n == 0 || d.dtype != key.dtype || d.bits != key.bits) continue;
         p.tile_start[m] = tiles;
         p.t[m] = make_d(d.data, d.n, d.packed, d.group_min, d.group_scale);
-        tiles += ceil_div(d.n, gact::kDequantTileElems);
+        tiles += gact::dequant_tiles(d.n);
         ++m;
       }
       if (m == 0) break;

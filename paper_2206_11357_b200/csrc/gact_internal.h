@@ -67,5 +67,11 @@ inline int64_t quantize_tiles(int64_t n, int log2g) {
   return (t + kTileAlign - 1) / kTileAlign * kTileAlign;
 }
 constexpr int64_t kDequantTileElems = 256;
+// Dequantize tile counts are rounded up to this (CTA units never straddle tensors).
+constexpr int64_t kDequantAlign = 32;
+inline int64_t dequant_tiles(int64_t n) {
+  const int64_t t = (n + kDequantTileElems - 1) / kDequantTileElems;
+  return (t + kDequantAlign - 1) / kDequantAlign * kDequantAlign;
+}
 
 }  // namespace gact

@@ -9,6 +9,7 @@ echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
 for dt in bf16 f32; do for b in 1 2 4 8; do
   python tools/prof_kernels.py --bits $b --dtype $dt --reps 1 2>&1 | tail -1
 done; done
+python tools/prof_kernels.py --bits 2 --reps 1 --ref 2>&1 | tail -2
 for d in build/var_*; do
   [ -f $d/libgact.so ] || continue
   echo "== $d"

@@ -15,6 +15,7 @@ p.add_argument("--dtype", default="bf16")
 p.add_argument("--n", type=int, default=1 << 28)
 p.add_argument("--G", type=int, default=256)
 p.add_argument("--reps", type=int, default=3)
+p.add_argument("--ref", action="store_true", help="also time torch fill_/copy_ (write / copy bandwidth)")
 a = p.parse_args()
 dt = {"bf16": torch.bfloat16, "f32": torch.float32, "f16": torch.float16}[a.dtype]
 x = torch.randn(a.n, device="cuda", dtype=torch.float32).to(dt)
@@ -41,3 +42,17 @@ st[1].record()
 torch.cuda.synchronize()
 td = st[0].elapsed_time(st[1]) / 10
 print(f"n={n} {a.dtype} b={b} G={a.G}: quantize {tq*1e3:.1f} us {qb/tq/1e6:.0f} GB/s | dequant {td*1e3:.1f} us {qb/td/1e6:.0f} GB/s")
+
+if a.ref:
+    buf = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
+    src = torch.empty_like(buf)
+    for name, fn, nbytes in [("fill_ (write)", lambda: buf.fill_(3), buf.numel()),
+                             ("copy_ (read+write)", lambda: buf.copy_(src), 2 * buf.numel())]:
+        fn()
+        st[0].record()
+        for r in range(10):
+            fn()
+        st[1].record()
+        torch.cuda.synchronize()
+        t = st[0].elapsed_time(st[1]) / 10
+        print(f"torch {name}: {t*1e3:.1f} us {nbytes/t/1e6:.0f} GB/s")
