@@ -229,6 +229,7 @@ def quantize_codes_span(x_span: np.ndarray, tag: int, n: int, G: int, bits: int,
     copy of those groups' elements (x_span = x[g0*G : min(g1*G, n)]). The oracle indexes the
     tensor by global element index; the base pointer is offset so that only the span is read."""
     x_span = np.ascontiguousarray(x_span).reshape(-1)
+    n, G, bits, seed, g0, g1 = int(n), int(G), int(bits), int(seed), int(g0), int(g1)
     count = min(g1 * G, n) - g0 * G
     assert x_span.size == count and g1 > g0
     base = x_span.ctypes.data - g0 * G * x_span.itemsize

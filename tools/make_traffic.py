@@ -26,7 +26,7 @@ for r in rows[i + 1:]:
     L["name"] = r[ix["Kernel Name"]]
     unit = r[ix["Metric Unit"]]
     v = float(r[ix["Metric Value"]].replace(",", ""))
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3}.get(unit, 1)
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "ns": 1e-9, "us": 1e-6, "ms": 1e-3}.get(unit, 1)
     L[r[ix["Metric Name"]]] = v * scale
 ids = sorted(launch)
 # one step = the first run of quantize launches followed by the dequantize launches

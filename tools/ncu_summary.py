@@ -37,11 +37,11 @@ def summary(path):
             u = units[hdr.index(k)]
             x = float(v.replace(",", ""))
             if "MB" in name:
-                x = x * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(u, 1.0)
+                x = x * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "KB": 1e-3, "MB": 1.0, "GB": 1e3}.get(u, 1.0)
             if name.startswith("duration"):
-                x = x * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(u, 1.0)
+                x = x * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}.get(u, 1.0)
             if name.startswith("SM clock"):
-                x = x * {"hz": 1e-9, "Khz": 1e-6, "Mhz": 1e-3, "Ghz": 1.0}.get(u, 1.0)
+                x = x * {"hz": 1e-9, "Khz": 1e-6, "Mhz": 1e-3, "Ghz": 1.0, "Hz": 1e-9, "GHz": 1.0}.get(u, 1.0)
             lines.append(f"  {name:24s} {x:,.3f}")
         stalls = {k.replace("smsp__pcsamp_warps_issue_stalled_", ""): float(d[k] or 0)
                   for k in hdr if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")}
