@@ -139,6 +139,37 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
   return v;
 }
 
+// ------------------------------------------------------------- mbarrier / bulk copy (TMA)
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar), "r"(parity) : "memory");
+}
+// One-dimensional bulk copy global -> shared through the TMA unit; completion is counted
+// in bytes on the mbarrier (complete_tx). src, dst 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+
 // 8 raw elements of one lane chunk: 32 bytes (f32) or 16 bytes (bf16 / f16).
 template <int DT>
 struct Raw8 {
@@ -152,6 +183,16 @@ template <>
 struct Raw8<DT_F16> {
   uint4 a;
 };
+
+template <int DT>
+__device__ __forceinline__ void lds8(Raw8<DT>& r, const unsigned char* p) {
+  if constexpr (DT == DT_F32) {
+    r.a = *reinterpret_cast<const uint4*>(p);
+    r.b = *reinterpret_cast<const uint4*>(p + 16);
+  } else {
+    r.a = *reinterpret_cast<const uint4*>(p);
+  }
+}
 
 template <int DT>
 __device__ __forceinline__ void load8(Raw8<DT>& r, const void* base, int64_t e) {
@@ -309,6 +350,12 @@ __device__ __forceinline__ PackedUnit<BITS> quantize_chunk(const float v[8], flo
 template <int DT, int BITS>
 __device__ __forceinline__ PackedUnit<BITS> quantize_chunk_raw(const Raw8<DT>& raw, float mn,
                                                                float inv, uint4 r) {
+#ifdef GACT_EXP_PHILOX_ONLY  // experiments only: cost of the random numbers alone
+  PackedUnit<BITS> o;
+  o.lo = r.x ^ r.y ^ r.z ^ r.w ^ raw.a.x ^ __float_as_uint(mn + inv);
+  o.hi = 0;
+  return o;
+#endif
   if constexpr (DT == DT_F32) {
     float v[8];
     widen8<DT>(raw, v);
