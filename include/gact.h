@@ -172,6 +172,19 @@ gact_status gact_allocate_bits(const double* sensitivity, const int64_t* numel, 
                                const int32_t* ladder, int32_t n_ladder, uint64_t budget_bits,
                                int32_t* bits_out);
 
+/* NEXT-3 — the reduction of Alg. 1: sum_i (a_i - b_i)^2 of two gradient
+ * vectors g0, g1 (one fwd+bwd each, seeds differing only for tensor l), from which
+ * c_l = 1/2 ||g0 - g1||^2 / S(b_l). Deterministic: a fixed grid of GACT_REDUCE_BLOCKS
+ * blocks writes binary64 partial sums in a fixed order, one block adds them in order, so
+ * the result is a pure function of (a, b, n) on any GPU.
+ *   a, b       device, n elements of `dtype` (gact_dtype), 16-byte aligned
+ *   partials   device, workspace of GACT_REDUCE_BLOCKS doubles (caller-owned)
+ *   out        device, out, one double (overwritten, not accumulated)
+ * Each element is widened exactly to binary64; (a - b)^2 accumulates in binary64. */
+#define GACT_REDUCE_BLOCKS 512
+gact_status gact_sq_diff_sum(const void* a, const void* b, int32_t dtype, int64_t n,
+                             double* partials, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -58,6 +58,7 @@ def lib() -> ctypes.CDLL:
             "oracle_predicted_variance": (ctypes.c_double, [P, P, i32]),
             "oracle_allocate_bits": (i32, [P, P, i32, P, i32, u64, P]),
             "oracle_allocate_bruteforce": (i32, [P, P, i32, P, i32, u64, P, P]),
+            "oracle_sq_diff_sum": (ctypes.c_double, [P, P, i32, i64]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -239,3 +240,11 @@ def quantize_codes_span(x_span: np.ndarray, tag: int, n: int, G: int, bits: int,
     _check(lib().oracle_quantize_codes(base, tag, n, G, bits, seed, g0, g1, _ptr(q), _ptr(mn),
                                        _ptr(sc)), "quantize_codes_span")
     return q, mn, sc
+
+
+def sq_diff_sum(a: np.ndarray, b: np.ndarray, tag: int) -> float:
+    """||a - b||^2 (Alg. 1's ||g0 - g1||^2); bf16 arrays as uint16 patterns with tag=BF16."""
+    a = np.ascontiguousarray(a).reshape(-1)
+    b = np.ascontiguousarray(b).reshape(-1)
+    assert a.size == b.size
+    return float(lib().oracle_sq_diff_sum(_ptr(a), _ptr(b), tag, a.size))

@@ -401,3 +401,17 @@ int32_t oracle_allocate_bruteforce(const double* c, const int64_t* D, int32_t L,
   if (value_out) *value_out = best;
   return ORACLE_OK;
 }
+
+/* ------------------------------------------------------------------------------------
+ * Alg. 1: c_l = 1/2 ||g0 - g1||^2 / S(b_l). The squared distance of the two
+ * gradient evaluations, each element widened exactly, differences and squares in long
+ * double, summed in index order.
+ * ---------------------------------------------------------------------------------- */
+double oracle_sq_diff_sum(const void* a, const void* b, int32_t dtype, int64_t n) {
+  long double acc = 0.0L;
+  for (int64_t i = 0; i < n; ++i) {
+    long double d = (long double)oracle_widen(a, dtype, i) - (long double)oracle_widen(b, dtype, i);
+    acc += d * d;
+  }
+  return (double)acc;
+}

@@ -82,6 +82,10 @@ int32_t oracle_allocate_bruteforce(const double* c, const int64_t* D, int32_t L,
                                    const int32_t* ladder, int32_t n_ladder, uint64_t B,
                                    int32_t* bits_out, double* value_out);
 
+/* sum_i (a_i - b_i)^2, the ||g0 - g1||^2 of Alg. 1, accumulated in long double
+ * (x86 80-bit) in index order. */
+double oracle_sq_diff_sum(const void* a, const void* b, int32_t dtype, int64_t n);
+
 #ifdef __cplusplus
 }
 #endif

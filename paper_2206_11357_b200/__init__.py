@@ -26,6 +26,7 @@ __all__ = [
     "lib", "GactError", "F32", "BF16", "F16", "DEFAULT_GROUP", "LADDER",
     "num_groups", "packed_words", "group_stats", "quantize_pack", "unpack_dequantize",
     "quantize_pack_batch", "unpack_dequantize_batch", "allocate_bits", "CompressedTensor",
+    "sq_diff_sum", "S",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -35,6 +36,7 @@ F32, BF16, F16 = 0, 1, 2
 DEFAULT_GROUP = 256
 LADDER = (1, 2, 4, 8)
 MAX_BATCH = 256
+REDUCE_BLOCKS = 512  # GACT_REDUCE_BLOCKS
 _TORCH_TAG = {torch.float32: F32, torch.bfloat16: BF16, torch.float16: F16}
 _TAG_TORCH = {v: k for k, v in _TORCH_TAG.items()}
 
@@ -81,6 +83,7 @@ def lib() -> ctypes.CDLL:
             "gact_quantize_pack_batch": (i32, [ctypes.POINTER(_Desc), i32, i32, P]),
             "gact_unpack_dequantize_batch": (i32, [ctypes.POINTER(_Desc), i32, i32, P]),
             "gact_allocate_bits": (i32, [P, P, i32, P, i32, u64, P]),
+            "gact_sq_diff_sum": (i32, [P, P, i32, i64, P, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -234,3 +237,23 @@ def allocate_bits(sensitivity, numel, budget_bits: int, ladder: Sequence[int] = 
     _check("gact_allocate_bits", lib().gact_allocate_bits(
         c.ctypes.data, D.ctypes.data, c.size, lad.ctypes.data, lad.size, int(budget_bits), out.ctypes.data))
     return out[:c.size]
+
+
+def S(b: int) -> float:
+    """S(b) = (2^b - 1)^-2 of P:479-480; S(32) = 0 (uncompressed)."""
+    return 0.0 if b == 32 else 1.0 / float((1 << b) - 1) ** 2
+
+
+def sq_diff_sum(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """||a - b||^2 as a 1-element float64 CUDA tensor (deterministic reduction in libgact;
+    the ||g0 - g1||^2 of Alg. 1)."""
+    _require_cuda(a, b)
+    if a.shape != b.shape or a.dtype != b.dtype:
+        raise ValueError("sq_diff_sum needs two tensors of the same shape and dtype")
+    a, b = a.contiguous(), b.contiguous()
+    partials = torch.empty(REDUCE_BLOCKS, dtype=torch.float64, device=a.device)  # caller-owned workspace
+    out = torch.empty(1, dtype=torch.float64, device=a.device)
+    _check("gact_sq_diff_sum", lib().gact_sq_diff_sum(
+        a.data_ptr(), b.data_ptr(), _TORCH_TAG[a.dtype], a.numel(), partials.data_ptr(),
+        out.data_ptr(), _stream(a)))
+    return out

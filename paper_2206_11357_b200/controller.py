@@ -1,0 +1,280 @@
+"""The GACT controller (§5): activation-compressed training on top of
+the libgact C ABI.
+
+  ctrl = Controller(model, avg_bits=4)           # P:571 "initialize the GACT controller"
+  def fwdbwdprop():                              # P:571-573 "instruct GACT how to perform
+      loss = loss_fn(model(x), y)                #  forward and backward propagation"
+      loss.backward()
+  ctrl.iterate(fwdbwdprop)                       # one training iteration (compressed context)
+  optimizer.step()
+
+* Capture: PyTorch saved-tensor hooks; pack_hook compresses every saved
+  context tensor, unpack_hook decompresses it in backward.
+* Filter: parameters (recorded data pointers) and tensors that do not require
+  gradients are kept as they are.
+* Dedup: a tensor saved by several ops (e.g. Q/K/V inputs) is compressed once per
+  iteration; the footprint is (data pointer, storage offset, shape, strides, version) plus a
+  weak reference to the first saver's tensor, so that a new tensor that reuses a freed
+  tensor's memory is never mistaken for it.
+* Bits (eqn:ilp P:471-475, greedy P:534): every `adapt_interval` iterations Alg. 1
+   estimates c_l for each context slot l from two gradient evaluations whose
+  compressor seeds differ only for tensor l, c_l = 1/2 ||g0 - g1||^2 / S(b_l); the
+  sensitivities are merged across data-parallel ranks (dist.merge_sensitivities) and the
+  greedy allocator of libgact assigns b_l under the budget avg_bits * sum_l D_l, with the
+  ladder {1, 2, 4, 8, 32} (32 = keep uncompressed).
+* Failure alert: the predicted compression variance V = sum_l c_l S(b_l) is
+  compared with the running variance of the gradient; a warning is raised when V dominates.
+
+Slots are identified by the order in which distinct context tensors are first saved in an
+iteration (a static graph saves the same tensors in the same order every iteration).
+All compression arithmetic runs in libgact's kernels; this module only routes tensors.
+"""
+from __future__ import annotations
+
+import math
+import warnings
+import weakref
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import dist as gdist
+
+SUPPORTED = (torch.float32, torch.bfloat16, torch.float16)
+LADDER = (1, 2, 4, 8, 32)
+RAW = 32
+
+
+def _splitmix64(x: int) -> int:
+    x = (x + 0x9E3779B97F4A7C15) & (2**64 - 1)
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & (2**64 - 1)
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & (2**64 - 1)
+    return x ^ (x >> 31)
+
+
+class LibgactBackend:
+    """Compression through libgact (the product path; CUDA tensors only)."""
+
+    def __init__(self, group_size: int = 256):
+        from . import quantize_pack  # noqa: F401  (loads libgact: fails loudly if missing)
+        self.group_size = group_size
+
+    def compress(self, t: torch.Tensor, bits: int, seed: int):
+        from . import quantize_pack
+        return quantize_pack(t, bits, seed, self.group_size)
+
+    def decompress(self, handle) -> torch.Tensor:
+        return handle.decompress()
+
+    def nbytes(self, handle) -> int:
+        return handle.nbytes()
+
+    def sq_diff(self, a: torch.Tensor, b: torch.Tensor) -> float:
+        from . import sq_diff_sum
+        return float(sq_diff_sum(a, b).item())
+
+
+@dataclass
+class Stats:
+    packed: int = 0          # context tensors compressed
+    raw: int = 0             # context tensors kept (filtered or at 32 bits)
+    dedup_hits: int = 0      # repeated saves of an already-compressed tensor
+    bytes_raw: int = 0       # bytes the compressed tensors would have taken
+    bytes_compressed: int = 0
+    alerts: list = field(default_factory=list)
+
+
+class Controller:
+    def __init__(self, model: torch.nn.Module, avg_bits: float = 4.0, group_size: int = 256,
+                 ladder=LADDER, adapt_interval: int = 100, est_bits: int = 4, seed: int = 0,
+                 min_numel: int = 256, alert_ratio: float = 1.0, backend=None, merge=True):
+        self.model = model
+        self.avg_bits = float(avg_bits)
+        self.ladder = tuple(int(b) for b in ladder)
+        self.adapt_interval = int(adapt_interval)
+        self.est_bits = int(est_bits)
+        self.seed = int(seed)
+        self.min_numel = int(min_numel)
+        self.alert_ratio = float(alert_ratio)
+        self.merge = merge
+        self.backend = backend if backend is not None else LibgactBackend(group_size)
+        self.param_ptrs = {p.data_ptr() for p in model.parameters()}
+        self.bits: list[int] = []        # b_l per slot (empty until the first adaptation)
+        self.numel: list[int] = []       # D_l per slot
+        self.sensitivity: np.ndarray | None = None
+        self.iteration = 0
+        self.stats = Stats()
+        self._seen: dict = {}
+        self._slot = 0
+        self._seed_of = None             # slot -> seed override (Alg. 1)
+        self._bits_override = None       # slot -> bits override (Alg. 1 estimation scheme)
+        self._grad_mean = None
+        self._grad_sq = None
+
+    # ---------------------------------------------------------------- capture hooks
+    def _footprint(self, t: torch.Tensor):
+        return (t.data_ptr(), t.storage_offset(), tuple(t.shape), tuple(t.stride()), t._version)
+
+    def _slot_bits(self, slot: int) -> int:
+        if self._bits_override is not None:
+            return self._bits_override(slot)
+        if slot < len(self.bits):
+            return self.bits[slot]
+        # before the first adaptation: the uniform scheme at the budget
+        below = [b for b in self.ladder if b != RAW and b <= self.avg_bits]
+        return max(below) if below else min(self.ladder)
+
+    def _slot_seed(self, slot: int) -> int:
+        if self._seed_of is not None:
+            return self._seed_of(slot)
+        return _splitmix64(_splitmix64(self.seed * 1_000_003 + self.iteration) ^ slot)
+
+    def pack_hook(self, t: torch.Tensor):
+        if (t.dtype not in SUPPORTED or not t.requires_grad or t.numel() < self.min_numel
+                or t.data_ptr() in self.param_ptrs):
+            self.stats.raw += 1
+            return ("raw", t)
+        fp = self._footprint(t)
+        hit = self._seen.get(fp)
+        if hit is not None and hit[0]() is not None:
+            # same footprint AND the first saver's tensor still alive: the very same tensor
+            # (a freed tensor's memory may be reused by a new one with the same footprint)
+            self.stats.dedup_hits += 1
+            return hit[1]
+        slot = self._slot
+        self._slot += 1
+        if slot >= len(self.numel):
+            self.numel.append(t.numel())
+        b = self._slot_bits(slot)
+        if b == RAW:
+            h = ("raw", t)
+            self.stats.raw += 1
+        else:
+            ct = self.backend.compress(t, b, self._slot_seed(slot))
+            h = ("q", ct, t.shape, t.dtype)
+            self.stats.packed += 1
+            self.stats.bytes_raw += t.numel() * t.element_size()
+            self.stats.bytes_compressed += self.backend.nbytes(ct)
+        self._seen[fp] = (weakref.ref(t), h)
+        return h
+
+    def unpack_hook(self, h):
+        if h[0] == "raw":
+            return h[1]
+        return self.backend.decompress(h[1]).view(h[2])
+
+    def hooks(self):
+        """Context manager installing the pack / unpack hooks ("install hooks")."""
+        self._seen = {}
+        self._slot = 0
+        return torch.autograd.graph.saved_tensors_hooks(self.pack_hook, self.unpack_hook)
+
+    # ---------------------------------------------------------------- gradients
+    def _params(self):
+        return [p for p in self.model.parameters() if p.requires_grad]
+
+    def _run(self, fwdbwdprop) -> torch.Tensor:
+        """One fwd+bwd under compression; returns the flattened fp32 gradient."""
+        for p in self._params():
+            p.grad = None
+        with self.hooks():
+            fwdbwdprop()
+        self._seen = {}
+        grads = [p.grad.reshape(-1).float() for p in self._params() if p.grad is not None]
+        return torch.cat(grads) if grads else torch.zeros(0)
+
+    # ---------------------------------------------------------------- Alg. 1
+    def estimate_sensitivity(self, fwdbwdprop, repeats: int = 1) -> np.ndarray:
+        """Alg. 1: c_l = 1/2 ||g0 - g1||^2 / S(b_l), where g0 seeds every Q^(l)
+        with r_l and g1 re-seeds only Q^(l) with r_{L+1}. The estimation scheme compresses
+        every slot at est_bits (Alg. 1 accepts any scheme b; under the linearisation c_l does
+        not depend on b). Averaged over `repeats` seed draws."""
+        saved_params = [p.grad for p in self._params()]
+        L = len(self.numel)
+        if L == 0:  # discover the slots with one pass
+            self._bits_override = lambda s: self.est_bits
+            self._run(fwdbwdprop)
+            self._bits_override = None
+            L = len(self.numel)
+        c = np.zeros(L)
+        b_est = self.est_bits
+        self._bits_override = lambda s: b_est
+        try:
+            for rep in range(repeats):
+                base = _splitmix64(self.seed ^ 0xA5A5A5A5 ^ (self.iteration << 20) ^ rep)
+                r = [_splitmix64(base + l + 1) for l in range(L + 1)]        # r_1 .. r_{L+1}
+                self._seed_of = lambda s: r[s] if s < L else r[L]
+                g0 = self._run(fwdbwdprop)
+                for l in range(L):
+                    self._seed_of = (lambda s, l=l: r[L] if s == l else (r[s] if s < L else r[L]))
+                    g1 = self._run(fwdbwdprop)
+                    c[l] += 0.5 * self.backend.sq_diff(g0, g1) / (1.0 / float((1 << b_est) - 1) ** 2)
+        finally:
+            self._seed_of = None
+            self._bits_override = None
+            for p, g in zip(self._params(), saved_params):
+                p.grad = g
+        return c / repeats
+
+    def adapt(self, fwdbwdprop, repeats: int = 1) -> list[int]:
+        """Refresh c (Alg. 1), merge it across ranks, and re-solve eqn:ilp."""
+        from . import allocate_bits
+        c = self.estimate_sensitivity(fwdbwdprop, repeats)
+        if self.merge:
+            c = gdist.merge_sensitivities(c, self.model_device())
+        self.sensitivity = c
+        D = np.asarray(self.numel, dtype=np.int64)
+        B = int(self.avg_bits * D.sum())
+        self.bits = [int(b) for b in allocate_bits(c, D, B, self.ladder)]
+        if self.merge:
+            gdist.assert_same_allocation(self.bits, self.model_device())
+        return self.bits
+
+    def model_device(self):
+        for p in self.model.parameters():
+            return p.device
+        return torch.device("cpu")
+
+    def predicted_variance(self) -> float:
+        """V(b) <= sum_l c_l S(b_l) (eqn:var-decomposition)."""
+        if self.sensitivity is None or not self.bits:
+            return float("nan")
+        return float(sum(c * (0.0 if b == RAW else 1.0 / float((1 << b) - 1) ** 2)
+                         for c, b in zip(self.sensitivity, self.bits)))
+
+    # ---------------------------------------------------------------- training iteration
+    def iterate(self, fwdbwdprop):
+        """One iteration (Fig. 2 "Line 19"): adapt every adapt_interval iterations, then run
+        fwdbwdprop with the compressed context; the parameters' .grad hold the AC gradient."""
+        if self.iteration % self.adapt_interval == 0:
+            self.adapt(fwdbwdprop)
+        for p in self._params():
+            p.grad = None
+        with self.hooks():
+            fwdbwdprop()
+        self._seen = {}
+        self._track_variance()
+        self.iteration += 1
+
+    def _track_variance(self, momentum: float = 0.9):
+        """Running mean / second moment of the gradient; alert when the predicted
+        compression variance dominates the gradient variance."""
+        grads = [p.grad.reshape(-1).float() for p in self._params() if p.grad is not None]
+        if not grads:
+            return
+        g = torch.cat(grads)
+        if self._grad_mean is None:
+            self._grad_mean, self._grad_sq = g.clone(), (g * g)
+            return
+        self._grad_mean.mul_(momentum).add_(g, alpha=1 - momentum)
+        self._grad_sq.mul_(momentum).add_(g * g, alpha=1 - momentum)
+        var = float((self._grad_sq - self._grad_mean ** 2).clamp_(min=0).sum().item())
+        V = self.predicted_variance()
+        if var > 0 and not math.isnan(V) and V / var > self.alert_ratio:
+            msg = f"GACT: predicted compression variance {V:.3g} exceeds {self.alert_ratio} x gradient variance {var:.3g}; raise the bit budget"
+            self.stats.alerts.append((self.iteration, V, var))
+            warnings.warn(msg, RuntimeWarning, stacklevel=3)
+
+    def compression_ratio(self) -> float:
+        return self.stats.bytes_raw / max(1, self.stats.bytes_compressed)

@@ -243,3 +243,19 @@ def test_unbiased_on_gpu(gact, orc):
     assert np.all(np.abs(mean - xh) <= tol)
     # Var[y] <= 1/4 range^2 S(b) = scale^2 / 4 (paper's B2 bound)
     assert np.all(var <= scale ** 2 / 4 * (1 + 6 / np.sqrt(N)) + 1e-30)
+
+
+@pytest.mark.parametrize("dtype", DTYPES, ids=["f32", "bf16", "f16"])
+def test_sq_diff_sum(gact, orc, dtype):
+    """||a - b||^2 (Alg. 1's reduction, NEXT-3) vs the oracle (long double, index order):
+    relative difference <= n 2^-52 (summation order only); bit-reproducible run to run."""
+    for n in [0, 1, 7, 8, 1000, 1 << 20, (1 << 22) + 13]:
+        a = make_input(n, dtype, seed=n + 1)
+        b = make_input(n, dtype, seed=n + 2)
+        got = gact.sq_diff_sum(a, b)
+        again = gact.sq_diff_sum(a, b)
+        torch.cuda.synchronize()
+        ref = orc.sq_diff_sum(oracle_input(a), oracle_input(b), TAGS[dtype])
+        g = float(got.item())
+        assert g == float(again.item())
+        assert abs(g - ref) <= max(n, 1) * 2.0 ** -52 * abs(ref) + 1e-300

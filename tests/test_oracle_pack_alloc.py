@@ -167,3 +167,28 @@ def test_monotone_dominance_scale(orc):
         bits = orc.allocate_bits(c, D, ladder, int(rng.integers(L * 50, 8 * L * 50)))[1]
         order = np.argsort(c)
         assert np.all(np.diff(bits[order]) >= 0)
+
+
+# ------------------------------------------------------------------ Alg. 1 reduction
+def test_sq_diff_sum_exact_small(orc):
+    """||a - b||^2 against exact rational arithmetic (Fractions), all dtypes."""
+    from fractions import Fraction
+    import torch
+    rng = np.random.default_rng(8)
+    for tag in (0, 1, 2):
+        for n in (0, 1, 7, 100, 1000):
+            a = rng.standard_normal(n).astype(np.float32) * 3
+            b = rng.standard_normal(n).astype(np.float32)
+            if tag == 1:
+                a = torch.from_numpy(a).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+                b = torch.from_numpy(b).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+                av = (a.astype(np.uint32) << 16).view(np.float32)
+                bv = (b.astype(np.uint32) << 16).view(np.float32)
+            elif tag == 2:
+                a, b = a.astype(np.float16).view(np.uint16), b.astype(np.float16).view(np.uint16)
+                av, bv = a.view(np.float16).astype(np.float32), b.view(np.float16).astype(np.float32)
+            else:
+                av, bv = a, b
+            exact = sum((Fraction(float(x)) - Fraction(float(y))) ** 2 for x, y in zip(av, bv))
+            got = orc.sq_diff_sum(a, b, tag)
+            assert abs(Fraction(got) - exact) <= Fraction(exact) * Fraction(1, 1 << 52) + Fraction(0)
