@@ -22,6 +22,11 @@ the libgact C ABI.
   sensitivities are merged across data-parallel ranks (dist.merge_sensitivities) and the
   greedy allocator of libgact assigns b_l under the budget avg_bits * sum_l D_l, with the
   ladder {1, 2, 4, 8, 32} (32 = keep uncompressed).
+* Swap / prefetch (optional `swap=True`): compressed tensors are copied to pinned
+  host memory on a swap-out stream right after compression (their device memory is released
+  once the copy is done); in backward, decompressing slot l first issues the host-to-device
+  copy of slot l - 1 (the next one backward needs) on a swap-in stream, and CUDA events
+  order the streams.
 * Failure alert: the predicted compression variance V = sum_l c_l S(b_l) is
   compared with the running variance of the gradient; a warning is raised when V dominates.
 
@@ -75,6 +80,45 @@ class LibgactBackend:
         return float(sq_diff_sum(a, b).item())
 
 
+class SwappedTensor:
+    """A compressed tensor parked in pinned host memory."""
+    __slots__ = ("host", "meta", "done", "dev", "ready")
+
+    def __init__(self, ct, swap_out: torch.cuda.Stream, pending: list):
+        cur = torch.cuda.current_stream(ct.packed.device)
+        swap_out.wait_stream(cur)                      # the codes are written
+        self.meta = (ct.shape, ct.dtype, ct.bits, ct.group_size, ct.seed, ct.packed.device)
+        dev = (ct.packed, ct.group_min, ct.group_scale)
+        with torch.cuda.stream(swap_out):
+            self.host = tuple(torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in dev)
+            for h, d in zip(self.host, dev):
+                h.copy_(d, non_blocking=True)
+            self.done = torch.cuda.Event()
+            self.done.record(swap_out)
+        pending.append((self.done, dev))               # device copies live until the D2H is done
+        self.dev = None
+        self.ready = None
+
+    def prefetch(self, swap_in: torch.cuda.Stream):
+        if self.dev is not None:
+            return
+        swap_in.wait_event(self.done)
+        with torch.cuda.stream(swap_in):
+            self.dev = tuple(h.to(self.meta[5], non_blocking=True) for h in self.host)
+            self.ready = torch.cuda.Event()
+            self.ready.record(swap_in)
+
+    def decompress(self, swap_in: torch.cuda.Stream) -> torch.Tensor:
+        from . import CompressedTensor
+        self.prefetch(swap_in)
+        cur = torch.cuda.current_stream(self.meta[5])
+        cur.wait_event(self.ready)
+        for t in self.dev:
+            t.record_stream(cur)
+        shape, dtype, bits, G, seed, _ = self.meta
+        return CompressedTensor(*self.dev, shape, dtype, bits, G, seed).decompress()
+
+
 @dataclass
 class Stats:
     packed: int = 0          # context tensors compressed
@@ -88,7 +132,8 @@ class Stats:
 class Controller:
     def __init__(self, model: torch.nn.Module, avg_bits: float = 4.0, group_size: int = 256,
                  ladder=LADDER, adapt_interval: int = 100, est_bits: int = 4, seed: int = 0,
-                 min_numel: int = 256, alert_ratio: float = 1.0, backend=None, merge=True):
+                 min_numel: int = 256, alert_ratio: float = 1.0, backend=None, merge=True,
+                 swap: bool = False):
         self.model = model
         self.avg_bits = float(avg_bits)
         self.ladder = tuple(int(b) for b in ladder)
@@ -111,6 +156,12 @@ class Controller:
         self._bits_override = None       # slot -> bits override (Alg. 1 estimation scheme)
         self._grad_mean = None
         self._grad_sq = None
+        self.swap = swap
+        self._swapped: dict = {}         # slot -> SwappedTensor (this iteration)
+        self._pending: list = []         # (event, device tensors) of swap-outs in flight
+        if swap:
+            self._swap_out = torch.cuda.Stream()
+            self._swap_in = torch.cuda.Stream()
 
     # ---------------------------------------------------------------- capture hooks
     def _footprint(self, t: torch.Tensor):
@@ -152,22 +203,48 @@ class Controller:
             self.stats.raw += 1
         else:
             ct = self.backend.compress(t, b, self._slot_seed(slot))
-            h = ("q", ct, t.shape, t.dtype)
+            if self.swap:
+                self._release_swapped()
+                st = SwappedTensor(ct, self._swap_out, self._pending)
+                self._swapped[slot] = st
+                h = ("s", st, t.shape, t.dtype, slot)
+            else:
+                h = ("q", ct, t.shape, t.dtype)
             self.stats.packed += 1
             self.stats.bytes_raw += t.numel() * t.element_size()
             self.stats.bytes_compressed += self.backend.nbytes(ct)
         self._seen[fp] = (weakref.ref(t), h)
         return h
 
+    def _release_swapped(self, wait: bool = False):
+        """Drop the device copies of compressed tensors whose swap-out copy has finished."""
+        keep = []
+        for ev, dev in self._pending:
+            if wait:
+                ev.synchronize()
+            elif not ev.query():
+                keep.append((ev, dev))
+        self._pending = keep
+
+    def flush(self):
+        """Wait for every swap-out and release the device copies (swap mode)."""
+        self._release_swapped(wait=True)
+
     def unpack_hook(self, h):
         if h[0] == "raw":
             return h[1]
+        if h[0] == "s":
+            prev = self._swapped.get(h[4] - 1)        # backward visits slots in reverse
+            if prev is not None:
+                prev.prefetch(self._swap_in)
+            return h[1].decompress(self._swap_in).view(h[2])
         return self.backend.decompress(h[1]).view(h[2])
 
     def hooks(self):
         """Context manager installing the pack / unpack hooks ("install hooks")."""
         self._seen = {}
         self._slot = 0
+        self._swapped = {}
         return torch.autograd.graph.saved_tensors_hooks(self.pack_hook, self.unpack_hook)
 
     # ---------------------------------------------------------------- gradients
