@@ -19,7 +19,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -84,48 +83,54 @@ def measured_peak():
 
 
 class ClockSampler:
-    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clocks and throttle reasons sampled DURING the timed region (NVML, every 5 ms, in a
+    thread started before the region; nvidia-smi as a fallback)."""
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap"}
 
     def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.stop = index, [], threading.Event()
+        self.active = threading.Event()
+        self.max_mhz = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def poll():
+                while not self.stop.is_set():
+                    if self.active.is_set():
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.rows.append((sm, rs))
+                    time.sleep(0.005)
+            self.thread = threading.Thread(target=poll, daemon=True)
             self.thread.start()
-        except FileNotFoundError:
-            self.proc = None
+        except Exception:
+            self.thread = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
+    def start(self):
+        self.active.set()
+
+    def end(self):
+        self.active.clear()
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({name for _, rs in self.rows for bit, name in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.rows), "source": "nvml, 5 ms, timed region only"}
 
 
 # ------------------------------------------------------------------------- our arm
@@ -136,10 +141,15 @@ def run_ours(args):
     from paper_2206_11357_b200 import dist as gdist
 
     rank, world, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())  # several ranks per GPU only in gloo tests
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    backend = os.environ.get("GACT_DIST_BACKEND", "nccl")  # gloo: functional test of the N > 1
+    if world > 1:                                           # path with several ranks on one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     gact.lib()
     dtype = {"bf16": torch.bfloat16, "f32": torch.float32, "f16": torch.float16}[args.dtype]
     s_in = torch.tensor([], dtype=dtype).element_size()
@@ -152,6 +162,7 @@ def run_ours(args):
     B = int(avg_bits * D.sum())
     c_local = synth.sensitivities(specs, seed=7, rank=rank)
     seeds_base = [synth.tensor_seed(2022, i, rank) for i in range(len(specs))]
+    seeds_np = np.array(seeds_base, dtype=np.uint64)
     # outputs sized for the widest code so that any allocation fits
     outs = [(torch.empty(gact.packed_words(int(n), 8), dtype=torch.int32, device=dev),
              torch.empty(gact.num_groups(int(n), G), dtype=torch.float32, device=dev),
@@ -159,17 +170,36 @@ def run_ours(args):
     ys = [torch.empty_like(x) for x in xs]
     stream = torch.cuda.current_stream(dev)
 
+    plans = {}
+
     def step(it, ev=None):
         c = gdist.merge_sensitivities(c_local, dev)                      # a7
         bits = gact.allocate_bits(c, D, B)                               # a6
-        seeds = [(s + it) & (2**64 - 1) for s in seeds_base]             # fresh rounding noise per step
+        key = bits.tobytes()
+        if os.environ.get("GACT_NO_PLAN"):
+            if ev:
+                ev[0].record(stream)
+            cts = gact.quantize_pack_batch(xs, bits.tolist(), [(s + it) & (2**64 - 1) for s in seeds_base], G, outs=[
+                (o[0][: gact.packed_words(int(n), int(b))], o[1], o[2]) for o, n, b in zip(outs, D, bits)])
+            if ev:
+                ev[1].record(stream)
+            gact.unpack_dequantize_batch(cts, outs=ys)
+            if ev:
+                ev[2].record(stream)
+            return bits
+        if key not in plans:                                             # descriptor tables per scheme
+            outs_b = [(o[0][: gact.packed_words(int(n), int(b))], o[1], o[2]) for o, n, b in zip(outs, D, bits)]
+            plans.clear()
+            plans[key] = (gact.BatchPlan("quantize", xs, outs_b, bits, G),
+                          gact.BatchPlan("dequantize", ys, outs_b, bits, G))
+        qplan, dplan = plans[key]
+        qplan.set_seeds(seeds_np + np.uint64(it))                        # fresh rounding noise per step
         if ev:
             ev[0].record(stream)
-        cts = gact.quantize_pack_batch(xs, bits.tolist(), seeds, G, outs=[
-            (o[0][: gact.packed_words(int(n), int(b))], o[1], o[2]) for o, n, b in zip(outs, D, bits)])
+        qplan.run()                                                      # a1-a3
         if ev:
             ev[1].record(stream)
-        gact.unpack_dequantize_batch(cts, outs=ys)                      # a4-a5
+        dplan.run()                                                      # a4-a5
         if ev:
             ev[2].record(stream)
         return bits
@@ -188,19 +218,23 @@ def run_ours(args):
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        if not os.environ.get("GACT_NO_CLOCKS"):
+            clk.start()
         t0.record(stream)
         for it in range(args.steps):
             bits = step(args.warmup + it, ev[it])
         t1.record(stream)
         torch.cuda.synchronize()
+        clk.end()
     if world > 1:
         dist.barrier()
     ms = t0.elapsed_time(t1)
     q_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
     d_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    red_dev = dev if backend == "nccl" else torch.device("cpu")
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)   # max over ranks of the device-timed region
         gdist.assert_same_allocation(bits, dev)
     ms_max = float(ms_t.item())
     step_bytes = qb + db
@@ -309,7 +343,8 @@ def run_e2e(args, gact, xs, D, B, c_local, seeds_base, G, s_in, dev, world):
     t1.record(stream)
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    red_dev = dev if world == 1 or torch.distributed.get_backend() == "nccl" else torch.device("cpu")
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
     qb = db = 0

@@ -26,7 +26,7 @@ __all__ = [
     "lib", "GactError", "F32", "BF16", "F16", "DEFAULT_GROUP", "LADDER",
     "num_groups", "packed_words", "group_stats", "quantize_pack", "unpack_dequantize",
     "quantize_pack_batch", "unpack_dequantize_batch", "allocate_bits", "CompressedTensor",
-    "sq_diff_sum", "S",
+    "sq_diff_sum", "S", "BatchPlan",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -257,3 +257,36 @@ def sq_diff_sum(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
         a.data_ptr(), b.data_ptr(), _TORCH_TAG[a.dtype], a.numel(), partials.data_ptr(),
         out.data_ptr(), _stream(a)))
     return out
+
+
+# numpy view of gact_tensor_desc (include/gact.h): 4 pointers, n, seed, bits, dtype = 56 bytes
+_DESC_NP = np.dtype([("data", np.uint64), ("packed", np.uint64), ("group_min", np.uint64),
+                     ("group_scale", np.uint64), ("n", np.int64), ("seed", np.uint64),
+                     ("bits", np.int32), ("dtype", np.int32)])
+assert _DESC_NP.itemsize == ctypes.sizeof(_Desc)
+
+
+class BatchPlan:
+    """A prepared batched call over fixed tensors and bits (the descriptor table is built once;
+    a step only rewrites the seeds). `kind` is "quantize" (xs are inputs, outs the
+    (packed, min, scale) triples) or "dequantize" (xs are outputs y, outs the triples read)."""
+
+    def __init__(self, kind: str, xs, outs, bits, group_size: int = DEFAULT_GROUP):
+        self.kind, self.group_size = kind, group_size
+        self.refs = (list(xs), list(outs))  # keep the tensors alive
+        self.table = np.zeros(len(xs), dtype=_DESC_NP)
+        for i, (x, (p, mn, sc), b) in enumerate(zip(xs, outs, bits)):
+            _require_cuda(x, p, mn, sc)
+            self.table[i] = (x.data_ptr(), p.data_ptr(), mn.data_ptr(), sc.data_ptr(), x.numel(), 0, int(b),
+                             _TORCH_TAG[x.dtype])
+        self.stream_of = xs[0] if len(xs) else None
+        self.fn = lib().gact_quantize_pack_batch if kind == "quantize" else lib().gact_unpack_dequantize_batch
+
+    def set_seeds(self, seeds) -> None:
+        self.table["seed"] = np.asarray(seeds, dtype=np.uint64)
+
+    def run(self) -> None:
+        if not len(self.table):
+            return
+        ptr = ctypes.cast(self.table.ctypes.data, ctypes.POINTER(_Desc))
+        _check(f"gact_{self.kind}_batch", self.fn(ptr, len(self.table), self.group_size, _stream(self.stream_of)))

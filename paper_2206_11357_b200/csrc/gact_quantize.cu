@@ -109,22 +109,6 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
   const int warp = threadIdx.x >> 5;
   const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
   const int64_t cunits = P.tiles_total / CU;
-  // The Philox blocks of a warp's unit: they depend only on the seed and the element index,
-  // so they are computed while the unit's loads are in flight. (Computing the NEXT unit's
-  // blocks one iteration ahead, or in separate producer warps fed by TMA, were both
-  // measured slower on B200: DESIGN.md §4.)
-  auto unit_rnd = [&](int64_t cu_, int cur_, uint4 (&r)[U][CPL]) {
-    const QTensor& Tn = P.t[cur_];
-    const int64_t eb = (cu_ * CU - P.tile_start[cur_]) * TE + (int64_t)warp * U * TE;
-    if (eb + U * TE <= Tn.n) {
-      const uint32_t k0 = (uint32_t)Tn.seed, k1 = (uint32_t)(Tn.seed >> 32);
-      const uint64_t blk = (uint64_t)(eb + lane * kChunk) >> 3;
-#pragma unroll
-      for (int k = 0; k < U; ++k)
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) r[k][c] = philox4x32_10(blk + (k * TE + c * kWarpTile) / kChunk, k0, k1);
-    }
-  };
   int cur = 0;
   // CTA-unit bookkeeping (tensor, seed, base pointers) depends only on blockIdx and the
   // loop counter: it lives in uniform registers.
@@ -143,8 +127,20 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
     for (int k = 0; k < U; ++k)
 #pragma unroll
       for (int c = 0; c < CPL; ++c) load8<DT>(raw[k][c], T.x, e_lane + k * TE + c * kWarpTile);
+    // The unit's Philox blocks depend only on the seed and the element index, so they are
+    // computed while the loads are in flight. (Computing the NEXT unit's blocks one
+    // iteration ahead, or in separate producer warps fed by TMA bulk copies, were both
+    // measured slower on B200: DESIGN.md §4.)
     uint4 rnd[U][CPL];
-    if constexpr (!STATS) unit_rnd(cu, cur, rnd);
+    if constexpr (!STATS) {
+      const uint32_t k0 = (uint32_t)T.seed, k1 = (uint32_t)(T.seed >> 32);
+      const uint64_t blk = (uint64_t)e_lane >> 3;
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c)
+          rnd[k][c] = philox4x32_10(blk + (k * TE + c * kWarpTile) / kChunk, k0, k1);
+    }
     float mnk[U], mxk[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
