@@ -315,11 +315,14 @@ __device__ __forceinline__ void code_pair(f2_t d2, f2_t inv2, uint32_t rw, uint3
   f2_split_bits(w2, w_lo, w_hi);
 }
 
+// Pack the low bytes q_j of w_j (= 0x4B00_0000 + q_j) into the chunk's 8*BITS-bit unit:
+// b = 8 by byte permutes; b < 8 by one IMAD per code (acc + (w_j << b j), mod 2^32), minus
+// the constant sum of the 0x4B00_0000 terms. (A byte-permute + funnel-shift packing that
+// keeps b < 8 in the integer pipe was measured slower: that pipe is as busy as the FMA pipe.)
 template <int BITS>
 __device__ __forceinline__ PackedUnit<BITS> pack_codes(const uint32_t w[8]) {
   PackedUnit<BITS> out;
   if constexpr (BITS == 8) {
-    // gather the low byte of each w_j (byte permutes)
     out.lo = __byte_perm(__byte_perm(w[0], w[1], 0x0040), __byte_perm(w[2], w[3], 0x0040), 0x5410);
     out.hi = __byte_perm(__byte_perm(w[4], w[5], 0x0040), __byte_perm(w[6], w[7], 0x0040), 0x5410);
   } else {
