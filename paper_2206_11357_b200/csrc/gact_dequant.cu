@@ -13,6 +13,7 @@
 #include "gact_device.cuh"
 #include "gact_internal.h"
 
+
 namespace gact {
 
 namespace {
@@ -86,9 +87,9 @@ __device__ __forceinline__ void decode8(uint2 u, float mn, float scale, float y[
 template <int DT>
 __device__ __forceinline__ void store8(void* ybase, int64_t e0, const float y[8]) {
   if constexpr (DT == DT_F32) {
-    float4* p = reinterpret_cast<float4*>(static_cast<float*>(ybase) + e0);
-    __stcs(p, make_float4(y[0], y[1], y[2], y[3]));
-    __stcs(p + 1, make_float4(y[4], y[5], y[6], y[7]));
+    float* p = static_cast<float*>(ybase) + e0;
+    __stcs(reinterpret_cast<float4*>(p), make_float4(y[0], y[1], y[2], y[3]));
+    __stcs(reinterpret_cast<float4*>(p) + 1, make_float4(y[4], y[5], y[6], y[7]));
   } else {
     uint32_t w[4];
 #pragma unroll
@@ -103,6 +104,59 @@ __device__ __forceinline__ void store8(void* ybase, int64_t e0, const float y[8]
     }
     uint4* p = reinterpret_cast<uint4*>(static_cast<uint16_t*>(ybase) + e0);
     __stcs(p, make_uint4(w[0], w[1], w[2], w[3]));
+  }
+}
+
+// 16 elements of one lane with 256-bit streaming stores (y 32-byte aligned): 32 bytes of
+// bf16 / f16 or 2 x 32 bytes of f32. Wide stores reach a markedly higher write bandwidth
+// than 128-bit ones on B200.
+__device__ __forceinline__ void st256(void* p, const uint32_t w[8]) {
+  asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(w[0]), "r"(w[1]),
+               "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]) : "memory");
+}
+
+template <int DT>
+__device__ __forceinline__ void store16(void* ybase, int64_t e0, const float y[16]) {
+  if constexpr (DT == DT_F32) {
+    float* p = static_cast<float*>(ybase) + e0;
+    st256(p, reinterpret_cast<const uint32_t*>(y));
+    st256(p + 8, reinterpret_cast<const uint32_t*>(y) + 8);
+  } else {
+    uint32_t w[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if constexpr (DT == DT_BF16) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(y[2 * q], y[2 * q + 1]);
+        w[q] = *reinterpret_cast<uint32_t*>(&h);
+      } else {
+        __half2 h = __floats2half2_rn(y[2 * q], y[2 * q + 1]);
+        w[q] = *reinterpret_cast<uint32_t*>(&h);
+      }
+    }
+    st256(static_cast<uint16_t*>(ybase) + e0, w);
+  }
+}
+
+// The packed codes of 16 consecutive elements (2*BITS bytes; packed 16-byte aligned) as the
+// units of their two 8-element halves.
+template <int BITS>
+__device__ __forceinline__ void load_unit16(const unsigned char* p, uint2& u0, uint2& u1) {
+  if constexpr (BITS == 1) {
+    const uint32_t v = __ldg(reinterpret_cast<const uint16_t*>(p));
+    u0 = make_uint2(v & 0xFFu, 0u);
+    u1 = make_uint2(v >> 8, 0u);
+  } else if constexpr (BITS == 2) {
+    const uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(p));
+    u0 = make_uint2(v & 0xFFFFu, 0u);
+    u1 = make_uint2(v >> 16, 0u);
+  } else if constexpr (BITS == 4) {
+    const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+    u0 = make_uint2(v.x, 0u);
+    u1 = make_uint2(v.y, 0u);
+  } else {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+    u0 = make_uint2(v.x, v.y);
+    u1 = make_uint2(v.z, v.w);
   }
 }
 
@@ -146,13 +200,15 @@ constexpr int kDequantUnit = GACT_D_UNIT;  // tiles per warp per unit
 static_assert(kDequantAlign % (kWarps * kDequantUnit) == 0, "CTA unit must divide the alignment");
 
 // CTAs walk units of 8 warps x U tiles (tensors padded to kDequantAlign tiles), so the
-// unit's tensor bookkeeping is CTA-uniform; a warp decodes U consecutive tiles.
-template <int DT, int BITS, int MAXB>
+// unit's tensor bookkeeping is CTA-uniform; a warp decodes U consecutive tiles of 32 x LE
+// elements (LE = 16: 256-bit stores, needs y 32-byte and packed 16-byte aligned; LE = 8:
+// 128-bit stores, the ABI's 16-byte alignment).
+template <int DT, int BITS, int MAXB, int LE>
 __global__ void __launch_bounds__(kThreads, GACT_D_MINB)
     dequantize_kernel(const __grid_constant__ DBatch<MAXB> P) {
   constexpr int U = kDequantUnit;
   constexpr int CU = kWarps * U;
-  constexpr int TE = (int)kDequantTileElems;
+  constexpr int TE = 32 * LE;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   int cur = 0;
@@ -161,29 +217,35 @@ __global__ void __launch_bounds__(kThreads, GACT_D_MINB)
     const DTensor& T = P.t[cur];
     const int64_t e_base = (cu * CU - P.tile_start[cur] + (int64_t)warp * U) * TE;
     if (e_base + U * TE > T.n) {
-      if (e_base < T.n) dequant_generic<DT, BITS>(T, e_base, U, P.log2g, lane);
+      if (e_base < T.n) dequant_generic<DT, BITS>(T, e_base, U * TE / (int)kDequantTileElems, P.log2g, lane);
       continue;
     }
-    const int64_t e_lane = e_base + lane * kChunk;
+    const int64_t e_lane = e_base + lane * LE;
     const unsigned char* src = reinterpret_cast<const unsigned char*>(T.packed) + (e_lane * BITS) / 8;
-    uint2 unit[U];
+    uint2 unit[U][LE / 8];
     float mn[U], sc[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       const unsigned char* p = src + (k * TE * BITS) / 8;
-      if constexpr (BITS == 1) unit[k] = make_uint2(__ldg(p), 0u);
-      else if constexpr (BITS == 2) unit[k] = make_uint2(__ldg(reinterpret_cast<const uint16_t*>(p)), 0u);
-      else if constexpr (BITS == 4) unit[k] = make_uint2(__ldg(reinterpret_cast<const uint32_t*>(p)), 0u);
-      else unit[k] = __ldg(reinterpret_cast<const uint2*>(p));
-      const int64_t g = (e_lane + k * TE) >> P.log2g;
+      if constexpr (LE == 16) {
+        load_unit16<BITS>(p, unit[k][0], unit[k][1]);
+      } else {
+        if constexpr (BITS == 1) unit[k][0] = make_uint2(__ldg(p), 0u);
+        else if constexpr (BITS == 2) unit[k][0] = make_uint2(__ldg(reinterpret_cast<const uint16_t*>(p)), 0u);
+        else if constexpr (BITS == 4) unit[k][0] = make_uint2(__ldg(reinterpret_cast<const uint32_t*>(p)), 0u);
+        else unit[k][0] = __ldg(reinterpret_cast<const uint2*>(p));
+      }
+      const int64_t g = (e_lane + k * TE) >> P.log2g;  // LE | G: one group per lane
       mn[k] = __ldg(T.group_min + g);
       sc[k] = __ldg(T.group_scale + g);
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      float y[8];
-      decode8<BITS>(unit[k], mn[k], sc[k], y);
-      store8<DT>(T.y, e_lane + k * TE, y);
+      float y[LE];
+#pragma unroll
+      for (int h = 0; h < LE / 8; ++h) decode8<BITS>(unit[k][h], mn[k], sc[k], y + 8 * h);
+      if constexpr (LE == 16) store16<DT>(T.y, e_lane + k * TE, y);
+      else store8<DT>(T.y, e_lane + k * TE, y);
     }
   }
 }
@@ -195,18 +257,36 @@ int max_blocks_per_sm(K kernel) {
   return b;
 }
 
-template <int DT, int BITS, int MAXB>
-cudaError_t launch_d(const DBatch<MAXB>& p, cudaStream_t s) {
-  constexpr auto kernel = dequantize_kernel<DT, BITS, MAXB>;
-  static const int per_sm = max_blocks_per_sm(kernel);
+template <auto Kernel, typename PB>
+cudaError_t launch_dk(const PB& p, cudaStream_t s) {
+  static const int per_sm = max_blocks_per_sm(Kernel);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t want = p.tiles_total / (kWarps * kDequantUnit);
   const int64_t cap = (int64_t)sms * per_sm;
   const int grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
-  kernel<<<grid, kThreads, 0, s>>>(p);
+  Kernel<<<grid, kThreads, 0, s>>>(p);
   return cudaGetLastError();
+}
+
+#ifndef GACT_D_WIDE16
+#define GACT_D_WIDE16 1  // 256-bit stores also for 2-byte outputs
+#endif
+
+template <int DT, int BITS, int MAXB>
+cudaError_t launch_d(const DBatch<MAXB>& p, cudaStream_t s) {
+  if (p.lane_elems == 16 && (DT == DT_F32 || GACT_D_WIDE16)) {
+    return launch_dk<dequantize_kernel<DT, BITS, MAXB, 16>>(p, s);
+  }
+  if (p.lane_elems == 16) {  // narrow kernel over a tile space counted for 16-element lanes
+    DBatch<MAXB> q = p;
+    q.lane_elems = 8;
+    for (int i = 0; i <= q.count; ++i) q.tile_start[i] *= 2;
+    q.tiles_total *= 2;
+    return launch_dk<dequantize_kernel<DT, BITS, MAXB, 8>>(q, s);
+  }
+  return launch_dk<dequantize_kernel<DT, BITS, MAXB, 8>>(p, s);
 }
 
 template <int DT, int MAXB>

@@ -81,6 +81,10 @@ DTensor make_d(void* y, int64_t n, const uint32_t* packed, const float* mn, cons
 
 gact_status from_cuda(cudaError_t e) { return e == cudaSuccess ? GACT_OK : GACT_ERR_CUDA; }
 
+// 256-bit stores / 128-bit code loads of the wide dequantize path need y 32-byte and packed
+// 16-byte aligned (PyTorch allocations are); otherwise the 16-byte path of the ABI is used.
+bool wide_ok(const void* y, const void* packed) { return aligned(y, 32) && aligned(packed, 16); }
+
 // ----------------------------------------------------------------------- batch helpers
 // Tensors are grouped by (dtype, bits) and each class is launched with one kernel.
 struct ClassKey {
@@ -179,9 +183,10 @@ gact_status gact_unpack_dequantize(const uint32_t* packed, const float* group_mi
   std::memset(&p, 0, sizeof(p));
   p.count = 1;
   p.log2g = l2;
+  p.lane_elems = wide_ok(y, packed) ? 16 : 8;
   p.t[0] = make_d(y, n, packed, group_min, group_scale);
   p.tile_start[0] = 0;
-  p.tiles_total = p.tile_start[1] = gact::dequant_tiles(n);
+  p.tiles_total = p.tile_start[1] = gact::dequant_tiles(n, p.lane_elems);
   return from_cuda(gact::launch_dequantize<1>(p, y_dtype, bits, static_cast<cudaStream_t>(stream)));
 }
 
@@ -241,14 +246,24 @@ gact_status gact_unpack_dequantize_batch(const gact_tensor_desc* descs, int32_t 
     while (i < count) {
       std::memset(&p, 0, offsetof(DBatch<gact::kMaxBatch>, tile_start));
       p.log2g = l2;
+      // the chunk of tensors this launch covers decides the lane width: wide if all aligned
       int32_t m = 0;
+      bool wide = true;
+      for (int32_t j = i; j < count && m < gact::kMaxBatch; ++j) {
+        const gact_tensor_desc& d = descs[j];
+        if (d.n == 0 || d.dtype != key.dtype || d.bits != key.bits) continue;
+        wide = wide && wide_ok(d.data, d.packed);
+        ++m;
+      }
+      p.lane_elems = wide ? 16 : 8;
+      m = 0;
       int64_t tiles = 0;
       for (; i < count && m < gact::kMaxBatch; ++i) {
         const gact_tensor_desc& d = descs[i];
         if (d.n == 0 || d.dtype != key.dtype || d.bits != key.bits) continue;
         p.tile_start[m] = tiles;
         p.t[m] = make_d(d.data, d.n, d.packed, d.group_min, d.group_scale);
-        tiles += gact::dequant_tiles(d.n);
+        tiles += gact::dequant_tiles(d.n, p.lane_elems);
         ++m;
       }
       if (m == 0) break;

@@ -43,6 +43,7 @@ template <int MAXB>
 struct DBatch {
   int32_t count;
   int32_t log2g;
+  int32_t lane_elems;  // 16: 256-bit stores (y 32-B, packed 16-B aligned); 8: 128-bit stores
   int64_t tiles_total;
   int64_t tile_start[MAXB + 1];
   DTensor t[MAXB];
@@ -66,11 +67,12 @@ inline int64_t quantize_tiles(int64_t n, int log2g) {
   const int64_t t = (n + te - 1) / te;
   return (t + kTileAlign - 1) / kTileAlign * kTileAlign;
 }
-constexpr int64_t kDequantTileElems = 256;
+constexpr int64_t kDequantTileElems = 256;  // the narrow (8-element lane) tile
 // Dequantize tile counts are rounded up to this (CTA units never straddle tensors).
 constexpr int64_t kDequantAlign = 32;
-inline int64_t dequant_tiles(int64_t n) {
-  const int64_t t = (n + kDequantTileElems - 1) / kDequantTileElems;
+inline int64_t dequant_tiles(int64_t n, int lane_elems) {
+  const int64_t te = 32 * lane_elems;
+  const int64_t t = (n + te - 1) / te;
   return (t + kDequantAlign - 1) / kDequantAlign * kDequantAlign;
 }
 

@@ -259,3 +259,23 @@ def test_sq_diff_sum(gact, orc, dtype):
         g = float(got.item())
         assert g == float(again.item())
         assert abs(g - ref) <= max(n, 1) * 2.0 ** -52 * abs(ref) + 1e-300
+
+
+@pytest.mark.parametrize("bits", BITS)
+def test_dequant_narrow_and_wide_paths_agree(gact, bits):
+    """The 256-bit-store path (y 32-byte, packed 16-byte aligned) and the ABI's 16-byte path
+    (taken for less-aligned buffers) write identical values."""
+    for dtype in DTYPES:
+        n = 256 * 40 + 77
+        x = make_input(n, dtype, seed=bits)
+        ct = gact.quantize_pack(x, bits, 5, 256)
+        wide = ct.decompress().reshape(-1)
+        es = torch.tensor([], dtype=dtype).element_size()
+        pad = 16 // es                                   # 16-byte offset: not 32-byte aligned
+        ybuf = torch.empty(n + pad, dtype=dtype, device="cuda")
+        pbuf = torch.zeros(ct.packed.numel() + 2, dtype=torch.int32, device="cuda")
+        pbuf[2:] = ct.packed                             # 8-byte offset: not 16-byte aligned
+        narrow = gact.unpack_dequantize(pbuf[2:], ct.group_min, ct.group_scale, n, bits, 256, dtype,
+                                        out=ybuf[pad:])
+        torch.cuda.synchronize()
+        assert torch.equal(narrow, wide)
