@@ -16,7 +16,7 @@
 //    loads are in flight (they depend only on (seed, element index)); the U groups'
 //    divisions run on U lanes and are broadcast with one shuffle.
 //  * G in {32, 64, 128}: a tile holds 256/G groups of G/8 lanes; segmented shuffles.
-//  * G in {2048, 4096}: two passes over the group (the second is served by L2).
+//  * G in {2048, 4096}: staged in shared memory (one HBM read).
 // A tensor's last tile may be partial (n % TE != 0): it takes the guarded generic path.
 #include <cfloat>
 
@@ -180,20 +180,25 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
 }
 
 // ---------------------------------------------------------------------------------------
-// G in {2048, 4096}: two passes over the group (the second is served by L2).
-template <int DT, int BITS, int MAXB, bool STATS>
-__global__ void __launch_bounds__(kThreads)
-    quantize_twopass_kernel(const __grid_constant__ QBatch<MAXB> P) {
+// G in {2048, 4096}: the group does not fit in registers. Pass 1 streams it from HBM once,
+// folding min/max and parking each lane's chunks in shared memory (G * s_in bytes per warp,
+// each lane re-reads only what it wrote: no synchronisation); pass 2 codes from shared memory.
+template <int DT, int BITS, int MAXB, bool STATS, int NW>
+__global__ void __launch_bounds__(NW * 32)
+    quantize_staged_kernel(const __grid_constant__ QBatch<MAXB> P) {
+  constexpr int ES = DT == DT_F32 ? 4 : 2;
+  extern __shared__ __align__(16) unsigned char stage_smem[];
   const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
   const int cpl = 1 << (P.log2g - 8);
   const int64_t TE = (int64_t)1 << P.log2g;
-  const int warp = threadIdx.x >> 5;
+  unsigned char* stage = stage_smem + (size_t)warp * (TE * ES) + lane * kChunk * ES;
   int cur = 0;
-  for (int64_t cu = blockIdx.x; cu < P.tiles_total / kWarps; cu += gridDim.x) {
-    cur = advance_cursor(P, cur, cu * kWarps);
+  for (int64_t cu = blockIdx.x; cu < P.tiles_total / NW; cu += gridDim.x) {
+    cur = advance_cursor(P, cur, cu * NW);
     const QTensor& T = P.t[cur];
-    const int64_t e0 = (cu * kWarps - P.tile_start[cur] + warp) * TE;
+    const int64_t e0 = (cu * NW - P.tile_start[cur] + warp) * TE;
     if (e0 >= T.n) continue;  // alignment padding of the tile space
     if (e0 + TE > T.n) {
       tile_generic<DT, BITS, STATS>(T, e0, P.log2g, Lf, lane);
@@ -205,7 +210,12 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
       for (int i = 0; i < 4; ++i) load8<DT>(raw[i], T.x, e0 + (c + i) * kWarpTile + lane * kChunk);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) chunk_minmax_raw<DT>(raw[i], lmn, lmx);
+      for (int i = 0; i < 4; ++i) {
+        chunk_minmax_raw<DT>(raw[i], lmn, lmx);
+        unsigned char* d = stage + (size_t)(c + i) * kWarpTile * ES;
+        *reinterpret_cast<uint4*>(d) = raw[i].a;
+        if constexpr (DT == DT_F32) *reinterpret_cast<uint4*>(d + 16) = raw[i].b;
+      }
     }
     const GroupParams gp = group_params(warp_min(lmn), warp_max(lmx), Lf);
     if (lane == 0) {
@@ -215,14 +225,13 @@ __global__ void __launch_bounds__(kThreads)
     if constexpr (!STATS) {
       const uint32_t k0 = (uint32_t)T.seed, k1 = (uint32_t)(T.seed >> 32);
       for (int c = 0; c < cpl; c += 4) {
-        Raw8<DT> raw[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) load8<DT>(raw[i], T.x, e0 + (c + i) * kWarpTile + lane * kChunk);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
+          Raw8<DT> raw;
+          lds8<DT>(raw, stage + (size_t)(c + i) * kWarpTile * ES);
           const int64_t e = e0 + (c + i) * kWarpTile + lane * kChunk;
           const uint4 r = philox4x32_10((uint64_t)e >> 3, k0, k1);
-          store_unit<BITS>(T.packed, e, quantize_chunk_raw<DT, BITS>(raw[i], gp.mn, gp.inv, r));
+          store_unit<BITS>(T.packed, e, quantize_chunk_raw<DT, BITS>(raw, gp.mn, gp.inv, r));
         }
       }
     }
@@ -292,12 +301,53 @@ __global__ void __launch_bounds__(kThreads)
         rnd[k] = philox4x32_10(((uint64_t)e_lane >> 3) + k * (kWarpTile / kChunk), (uint32_t)T.seed,
                                (uint32_t)(T.seed >> 32));
     }
+    if (e_warp + U * kWarpTile > T.n) {  // the tensor's last unit: tile by tile, guarded
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t t0 = e_warp + k * kWarpTile;
+        if (t0 >= T.n) break;  // warp-uniform: the rest of the unit is padding
+        small_tile<DT, BITS, STATS>(T, e_lane + k * kWarpTile, t0 + kWarpTile <= T.n, raw[k], rnd[k],
+                                    P.log2g, lpg, Lf, lane);
+      }
+      continue;
+    }
+    // Full unit: segmented butterflies give every lane its group's (min, max) for the U tiles;
+    // the U divisions of a group run on U different lanes of its segment (lpg >= 4 = U) and
+    // are broadcast back with one shuffle per tile.
+    float mnk[U], mxk[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      const int64_t t0 = e_warp + k * kWarpTile;
-      if (t0 >= T.n) break;  // warp-uniform: the rest of the unit is padding
-      small_tile<DT, BITS, STATS>(T, e_lane + k * kWarpTile, t0 + kWarpTile <= T.n, raw[k], rnd[k],
-                                  P.log2g, lpg, Lf, lane);
+      float lmn = FLT_MAX, lmx = -FLT_MAX;
+      chunk_minmax_raw<DT>(raw[k], lmn, lmx);
+      for (int o = 1; o < lpg; o <<= 1) {
+        lmn = fminf(lmn, __shfl_xor_sync(kFull, lmn, o));
+        lmx = fmaxf(lmx, __shfl_xor_sync(kFull, lmx, o));
+      }
+      mnk[k] = lmn;
+      mxk[k] = lmx;
+    }
+    const int sl = lane & (lpg - 1);  // lane within its group's segment
+    const int sel = sl & (U - 1);
+    float a = mnk[0], b = mxk[0];
+#pragma unroll
+    for (int k = 1; k < U; ++k) {
+      a = (sel == k) ? mnk[k] : a;
+      b = (sel == k) ? mxk[k] : b;
+    }
+    const GroupParams gp = group_params(a, b, Lf);
+    if (sl < U) {  // segment lane k stores tile k's group
+      const int64_t g = (e_lane + sl * kWarpTile) >> P.log2g;
+      T.group_min[g] = gp.mn;
+      T.group_scale[g] = gp.scale;
+    }
+    if constexpr (!STATS) {
+      unsigned char* out = reinterpret_cast<unsigned char*>(T.packed) + (e_lane * BITS) / 8;
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const float inv = __shfl_sync(kFull, gp.inv, (lane & ~(lpg - 1)) + k);
+        const float mn = __fadd_rn(mnk[k], 0.0f);
+        store_unit_at<BITS>(out + (k * kWarpTile * BITS) / 8, quantize_chunk_raw<DT, BITS>(raw[k], mn, inv, rnd[k]));
+      }
     }
   }
 }
@@ -328,6 +378,33 @@ cudaError_t launch_persistent(const PB& p, int64_t tiles_per_warp_iter, cudaStre
   return cudaGetLastError();
 }
 
+template <int DT, int BITS, int MAXB, bool STATS, int NW>
+cudaError_t launch_staged_nw(const QBatch<MAXB>& p, int smem, cudaStream_t s) {
+  constexpr auto kernel = quantize_staged_kernel<DT, BITS, MAXB, STATS, NW>;
+  static int configured = 0;  // largest dynamic smem size enabled so far
+  if (smem > configured) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = smem;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, NW * 32, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  const int64_t want = p.tiles_total / NW;
+  const int64_t cap = (int64_t)sm_count() * per_sm;
+  const int grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
+  kernel<<<grid, NW * 32, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+// 8 warps per CTA while a warp's stage is <= 8 KB; 4 warps for 16 KB stages (fp32, G = 4096)
+// so that several CTAs fit an SM.
+template <int DT, int BITS, int MAXB, bool STATS>
+cudaError_t launch_staged(const QBatch<MAXB>& p, cudaStream_t s) {
+  const int per_warp = (1 << p.log2g) * (DT == DT_F32 ? 4 : 2);
+  if (per_warp > 8192) return launch_staged_nw<DT, BITS, MAXB, STATS, 4>(p, 4 * per_warp, s);
+  return launch_staged_nw<DT, BITS, MAXB, STATS, kWarps>(p, kWarps * per_warp, s);
+}
+
 template <int DT, int BITS, int MAXB, bool STATS>
 cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
   switch (p.log2g) {
@@ -340,7 +417,7 @@ cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
     case 10:
       return launch_persistent<quantize_big_kernel<DT, BITS, 4, MAXB, STATS>>(p, kQuantUnit > 4 ? kQuantUnit / 4 : 1, s);
     default:
-      return launch_persistent<quantize_twopass_kernel<DT, BITS, MAXB, STATS>>(p, 1, s);
+      return launch_staged<DT, BITS, MAXB, STATS>(p, s);
   }
 }
 

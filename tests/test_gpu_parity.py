@@ -221,27 +221,34 @@ def test_batch_equals_single(gact, G):
 
 
 def test_unbiased_on_gpu(gact, orc):
-    """E[Q(x)] = x: 20000 seeds over the C1 tensor; the GPU mean of the decoded
-    values is within 4 sigma (+ the 2^-17 lane bias) of mn + t * scale, with t the
-    oracle's binary32 transform, and of x itself up to the transform's rounding."""
-    G, bits, N = 256, 2, 20000
-    xh = synth.c1_tensor(bits, G)[:1024]
+    """E[Q(x)] = x over 10^5 seeds of the C1 tensor: the GPU mean of
+    the decoded values is within 4.5 sigma (+ the 2^-17 lane bias) of x, and the per-element
+    variance never exceeds the paper's bound 1/4 range^2 S(b) = scale^2 / 4 (B2).
+    Seeds are batched 256 per launch (one descriptor per seed, same input)."""
+    G, bits, N, per = 256, 2, 100_000, 256
+    xh = synth.c1_tensor(bits, G)
     x = torch.from_numpy(xh).cuda()
-    acc = torch.zeros(x.numel(), dtype=torch.float64, device="cuda")
+    n = x.numel()
+    acc = torch.zeros(n, dtype=torch.float64, device="cuda")
     acc2 = torch.zeros_like(acc)
-    for s in range(N):
-        y = gact.quantize_pack(x, bits, s, G).decompress().double()
-        acc += y
-        acc2 += y * y
+    done = 0
+    while done < N:
+        m = min(per, N - done)
+        cts = gact.quantize_pack_batch([x] * m, [bits] * m, list(range(done, done + m)), G)
+        ys = torch.stack(gact.unpack_dequantize_batch(cts)).double()
+        acc += ys.sum(0)
+        acc2 += (ys * ys).sum(0)
+        done += m
     mean = (acc / N).cpu().numpy()
     var = (acc2 / N).cpu().numpy() - mean ** 2
     mn, sc = orc.group_stats(xh, 0, G, bits)
-    scale = np.repeat(sc.astype(np.float64), G)[: xh.size]
-    p = np.clip((xh.astype(np.float64) - np.repeat(mn, G)[: xh.size]) / np.maximum(scale, 1e-300) % 1.0, 0, 1)
+    scale = np.repeat(sc.astype(np.float64), G)[: n]
+    lo = np.repeat(mn.astype(np.float64), G)[: n]
+    t = np.where(scale > 0, (xh.astype(np.float64) - lo) / np.maximum(scale, 1e-300), 0.0)
+    p = t - np.floor(t)
     sig = np.sqrt(np.maximum(p * (1 - p), 1e-12) / N) * scale
-    tol = 4 * sig + (2.0 ** -17 + 1e-6) * scale + 4 * np.spacing(np.abs(xh)).astype(np.float64)
+    tol = 4.5 * sig + (2.0 ** -17 + 1e-6) * scale + 4 * np.spacing(np.abs(xh)).astype(np.float64)
     assert np.all(np.abs(mean - xh) <= tol)
-    # Var[y] <= 1/4 range^2 S(b) = scale^2 / 4 (paper's B2 bound, P:479-480)
     assert np.all(var <= scale ** 2 / 4 * (1 + 6 / np.sqrt(N)) + 1e-30)
 
 
