@@ -237,3 +237,62 @@ def test_checkpoint_segments_cb1(ctl):
     g = torch.cat([p.grad.reshape(-1) for p in model.parameters()])
     assert c.stats.packed > 0 and torch.isfinite(g).all()
     assert float((g - ref).norm() / ref.norm()) < 0.2
+
+
+def test_training_converges_like_fp32(ctl):
+    """§6.2 analog (SPEC acceptance 8): an MLP trained with the compressed context (adaptive
+    bits, average 4 and 2) reaches the accuracy of uncompressed training on a synthetic
+    Gaussian-mixture task (same initialisation, data order and steps)."""
+    def run(avg_bits):
+        g = torch.Generator(device="cuda").manual_seed(0)
+        centers = torch.randn(16, 64, device="cuda", generator=g) * 1.5
+        def batch():
+            y = torch.randint(0, 16, (512,), device="cuda", generator=g)
+            return centers[y] + torch.randn(512, 64, device="cuda", generator=g), y
+        m = mlp([64, 512, 512, 16], act=torch.nn.ReLU, seed=1)
+        opt = torch.optim.SGD(m.parameters(), lr=0.05, momentum=0.9)
+        c = None if avg_bits is None else ctl.Controller(m, avg_bits=avg_bits, ladder=(1, 2, 4, 8), merge=False,
+                                                         adapt_interval=100, seed=3)
+        for it in range(300):
+            x, y = batch()
+            f = fwdbwd(m, x, y)
+            if c is None:
+                opt.zero_grad()
+                f()
+            else:
+                c.iterate(f)
+            opt.step()
+        x, y = batch()
+        with torch.no_grad():
+            return float((m(x).argmax(1) == y).float().mean())
+    acc32, acc4, acc2 = run(None), run(4), run(2)
+    assert acc32 > 0.9
+    assert acc4 >= acc32 - 0.015, (acc32, acc4)
+    assert acc2 >= acc32 - 0.03, (acc32, acc2)
+
+
+def test_resnet18_context(ctl):
+    """A torchvision ResNet-18 (conv, BN, in-place ReLU, max-pool with int64 indices kept raw)
+    under the controller. Gradients stay aligned with the uncompressed ones and the error
+    shrinks with the bits (ReLU backward masks with the SAVED result, a nonlinear use of the
+    context: values within one step of 0 may decode to 0, so the error is not zero-mean)."""
+    torchvision = pytest.importorskip("torchvision")
+    torch.manual_seed(0)
+    m = torchvision.models.resnet18(num_classes=10).cuda().train()
+    x = torch.randn(32, 3, 64, 64, device="cuda")
+    y = torch.randint(0, 10, (32,), device="cuda")
+    f = fwdbwd(m, x, y)
+    m.zero_grad()
+    f()
+    ref = grads(m).clone()
+    err, cos = {}, {}
+    for b in (4, 8):
+        c = ctl.Controller(m, avg_bits=b, ladder=(b,), merge=False, adapt_interval=10**9)
+        c.iteration = 1
+        c.iterate(f)
+        g = grads(m)
+        err[b] = float((g - ref).norm() / ref.norm())
+        cos[b] = float(torch.nn.functional.cosine_similarity(g, ref, dim=0))
+        assert c.stats.packed > 20 and c.stats.raw > 0
+        assert c.compression_ratio() > (32 / (b + 0.25)) * 0.9
+    assert err[8] < err[4] and cos[8] > 0.97 and cos[4] > 0.5, (err, cos)
