@@ -260,7 +260,10 @@ def run_ours(args):
 
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, gact, xs, D, B, c_local, seeds_base, G, s_in, dev, world)
+        try:
+            e2e = run_e2e(args, gact, xs, D, B, c_local, seeds_base, G, s_in, dev, world)
+        except (RuntimeError, MemoryError) as exc:  # e.g. pinned host memory exhausted
+            e2e = {"value": None, "unit": "GB/s", "error": str(exc)[:200]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
