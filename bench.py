@@ -172,9 +172,18 @@ def run_ours(args):
 
     plans = {}
 
+    host_t = {"allreduce_s": 0.0, "alloc_s": 0.0, "n": 0}
+
     def step(it, ev=None):
-        c = gdist.merge_sensitivities(c_local, dev)                      # a7
+        t_a = time.perf_counter()
+        c = gdist.merge_sensitivities(c_local, dev)                      # a7 (returns host c)
+        t_b = time.perf_counter()
         bits = gact.allocate_bits(c, D, B)                               # a6
+        t_c = time.perf_counter()
+        if ev:
+            host_t["allreduce_s"] += t_b - t_a
+            host_t["alloc_s"] += t_c - t_b
+            host_t["n"] += 1
         key = bits.tobytes()
         if os.environ.get("GACT_NO_PLAN"):
             if ev:
@@ -274,16 +283,19 @@ def run_ours(args):
         "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": args.dtype, "data": "synthetic (seeded; shapes of the paper's workloads, DESIGN.md §6)",
+        "dtype": "f32", "data": "synthetic (seeded; shapes of the paper's workloads, DESIGN.md §6)",
         "config": {
             "workload": WORKLOAD_CONFIG.get(args.workload, args.workload), "tensors": len(specs),
+            "input_dtype": args.dtype, "arithmetic": "binary32 (codes, stats, dequantize); binary64 allocator",
             "elements_per_rank": int(D.sum()), "group_size": G, "avg_bits_budget": avg_bits,
             "bits_histogram": {str(k): v for k, v in sorted(classes.items())},
             "bytes_per_step_per_rank": int(step_bytes),
             "l2": "inputs %.1f GB per rank > 126 MB L2: no flush needed" % (D.sum() * s_in / 1e9),
             "parallelism": f"dp{world} (per-rank compression + NCCL all-reduce of c)",
         },
-        "phases": {"quantize_ms": round(q_ms, 4), "dequantize_ms": round(d_ms, 4),
+        "phases": {"allreduce_us": round(host_t["allreduce_s"] / max(1, host_t["n"]) * 1e6, 1),
+                   "allocate_us": round(host_t["alloc_s"] / max(1, host_t["n"]) * 1e6, 1),
+                   "quantize_ms": round(q_ms, 4), "dequantize_ms": round(d_ms, 4),
                    "quantize_gbs": round(q_gbs, 1), "dequantize_gbs": round(d_gbs, 1),
                    "quantize_frac": round(q_gbs / peak, 4), "dequantize_frac": round(d_gbs / peak, 4)},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
@@ -453,7 +465,7 @@ def run_reference(args):
         "impl": "reference", "metric": "quantize+pack / dequant GB/s per B200 (% of HBM peak); activation compression",
         "value": round(val, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(secs / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (seeded)",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded)",
         "config": {"workload": WORKLOAD_CONFIG.get(args.workload, args.workload), "group_size": G,
                    "avg_bits_budget": avg_bits, "sample": sample},
         "cpu_baseline": {"value": round(val, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
