@@ -19,17 +19,32 @@ def _active() -> bool:
     return dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
 
 
+_side_streams: dict = {}
+
+
 def merge_sensitivities(c_local, device=None) -> np.ndarray:
-    """All-reduce(SUM) / world of the local sensitivity vector (float64, L entries)."""
+    """All-reduce(SUM) / world of the local sensitivity vector (float64, L entries).
+
+    With NCCL the exchange runs on a dedicated side stream, so that waiting for the merged
+    vector (the allocator runs on the host) does not wait for the compute stream's queue."""
     c = np.ascontiguousarray(c_local, dtype=np.float64)
     if not _active():
         return c
     backend = dist.get_backend()
-    dev = device if (backend == "nccl" and device is not None) else torch.device("cpu")
-    t = torch.from_numpy(c).to(dev)
+    if backend == "nccl" and device is not None:
+        side = _side_streams.get(device)
+        if side is None:
+            side = _side_streams[device] = torch.cuda.Stream(device)
+        with torch.cuda.stream(side):
+            t = torch.from_numpy(c).to(device, non_blocking=False)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            t /= dist.get_world_size()
+            out = t.cpu().numpy()
+        return out
+    t = torch.from_numpy(c)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     t /= dist.get_world_size()
-    return t.cpu().numpy()
+    return t.numpy()
 
 
 def allocation_digest(bits) -> int:
