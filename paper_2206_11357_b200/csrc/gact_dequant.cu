@@ -190,6 +190,11 @@ __device__ __noinline__ void dequant_generic(const DTensor T, int64_t e_first, i
   }
 }
 
+// Grid = waves x resident CTAs: many waves (CTAs take units dynamically) reach a far higher
+// write bandwidth than a persistent grid (bf16 ResNet-50 set: 5.8 -> 6.6 TB/s).
+#ifndef GACT_D_WAVES
+#define GACT_D_WAVES 32
+#endif
 #ifndef GACT_D_UNIT
 #define GACT_D_UNIT 4
 #endif
@@ -264,7 +269,7 @@ cudaError_t launch_dk(const PB& p, cudaStream_t s) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t want = p.tiles_total / (kWarps * kDequantUnit);
-  const int64_t cap = (int64_t)sms * per_sm;
+  const int64_t cap = (int64_t)sms * per_sm * GACT_D_WAVES;
   const int grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
   Kernel<<<grid, kThreads, 0, s>>>(p);
   return cudaGetLastError();

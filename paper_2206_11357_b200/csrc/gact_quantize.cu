@@ -90,6 +90,12 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 // ---------------------------------------------------------------------------------------
 // G in {256, 512, 1024}: CPL = G/256 chunks per lane, U = kQuantUnit/CPL tiles per unit,
 // all in registers.
+// Grid = waves x resident CTAs. Several waves (CTAs pick up units dynamically as others
+// retire) beat a persistent grid for the FMA-bound 2-byte inputs (+6% at bf16); fp32 inputs
+// (HBM-bound) keep the persistent grid. Measured on B200: DESIGN.md §4.
+#ifndef GACT_Q_WAVES
+#define GACT_Q_WAVES 8
+#endif
 #ifndef GACT_Q_UNIT
 #define GACT_Q_UNIT 4
 #endif
@@ -368,11 +374,11 @@ inline int sm_count() {
 }
 
 template <auto Kernel, typename PB>
-cudaError_t launch_persistent(const PB& p, int64_t tiles_per_warp_iter, cudaStream_t s) {
+cudaError_t launch_persistent(const PB& p, int64_t tiles_per_warp_iter, cudaStream_t s, int waves = 1) {
   static const int per_sm = max_blocks_per_sm(Kernel);  // one cache per kernel
   const int64_t want = (p.tiles_total + (int64_t)kWarps * tiles_per_warp_iter - 1) /
                        ((int64_t)kWarps * tiles_per_warp_iter);
-  const int64_t cap = (int64_t)sm_count() * per_sm;
+  const int64_t cap = (int64_t)sm_count() * per_sm * waves;
   const int grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
   Kernel<<<grid, kThreads, 0, s>>>(p);
   return cudaGetLastError();
@@ -407,15 +413,16 @@ cudaError_t launch_staged(const QBatch<MAXB>& p, cudaStream_t s) {
 
 template <int DT, int BITS, int MAXB, bool STATS>
 cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
+  const int waves = DT == DT_F32 ? 1 : GACT_Q_WAVES;
   switch (p.log2g) {
     case 5: case 6: case 7:
-      return launch_persistent<quantize_small_kernel<DT, BITS, MAXB, STATS>>(p, 4, s);
+      return launch_persistent<quantize_small_kernel<DT, BITS, MAXB, STATS>>(p, 4, s, waves);
     case 8:
-      return launch_persistent<quantize_big_kernel<DT, BITS, 1, MAXB, STATS>>(p, kQuantUnit, s);
+      return launch_persistent<quantize_big_kernel<DT, BITS, 1, MAXB, STATS>>(p, kQuantUnit, s, waves);
     case 9:
-      return launch_persistent<quantize_big_kernel<DT, BITS, 2, MAXB, STATS>>(p, kQuantUnit / 2, s);
+      return launch_persistent<quantize_big_kernel<DT, BITS, 2, MAXB, STATS>>(p, kQuantUnit / 2, s, waves);
     case 10:
-      return launch_persistent<quantize_big_kernel<DT, BITS, 4, MAXB, STATS>>(p, kQuantUnit > 4 ? kQuantUnit / 4 : 1, s);
+      return launch_persistent<quantize_big_kernel<DT, BITS, 4, MAXB, STATS>>(p, kQuantUnit > 4 ? kQuantUnit / 4 : 1, s, waves);
     default:
       return launch_staged<DT, BITS, MAXB, STATS>(p, s);
   }
