@@ -33,10 +33,59 @@ __device__ __forceinline__ uint32_t xor3(uint32_t a, uint32_t b, uint32_t c) {
   return d;
 }
 
+// hi32(a * m) on the FP64 pipe: with A = 2^52 + a (bit pattern {a, 0x43300000}, no
+// conversion), fma.rm(A, m 2^-32, 2^52 - 2^20 m) = 2^52 + a m 2^-32 exactly before one
+// rounding toward -inf at unit spacing, i.e. 2^52 + floor(a m / 2^32): the result's low
+// word is hi32(a m) and its high word is 0x43300000 again, so the next round's operand
+// {xor, that high word} needs no move. B200 runs DFMA at 64 lanes/clk/SM on its own pipe,
+// which takes the upper half of each 32x32->64 product off the FMA-heavy pipe (the low
+// half stays one IMAD).
+template <uint32_t M>
+__device__ __forceinline__ void mul_hi_f64(uint32_t a, uint32_t h, uint32_t& hi, uint32_t& h_out) {
+  constexpr double kScale = (double)M * (1.0 / 4294967296.0);
+  constexpr double kBias = 4503599627370496.0 - (double)M * 1048576.0;
+  asm("{\n\t.reg .f64 A, R;\n\tmov.b64 A, {%2, %3};\n\tfma.rm.f64 R, A, %4, %5;\n\t"
+      "mov.b64 {%0, %1}, R;\n\t}"
+      : "=r"(hi), "=r"(h_out)
+      : "r"(a), "r"(h), "d"(kScale), "d"(kBias));
+}
+
+#ifndef GACT_PHILOX_F64
+#define GACT_PHILOX_F64 0  // 1: upper product halves on the FP64 pipe (see mul_hi_f64)
+#endif
+
 #ifndef GACT_EXP_ROUNDS
 #define GACT_EXP_ROUNDS 10  // experiments only: Philox4x32-10 is the defined generator
 #endif
 __device__ __forceinline__ uint4 philox4x32_10(uint64_t block, uint32_t k0, uint32_t k1) {
+#if GACT_PHILOX_F64
+  // Round 0 has c2 = c3 = 0 (so M1 c2 = 0); later rounds carry the FP64 high words.
+  uint32_t c1 = (uint32_t)(block >> 32), c3, hi0, h0, h2;
+  const uint32_t a0 = (uint32_t)block;
+  mul_hi_f64<0xD2511F53u>(a0, 0x43300000u, hi0, h2);
+  c3 = a0 * 0xD2511F53u;
+  uint32_t c0 = c1 ^ k0, c2 = hi0 ^ k1;
+  c1 = 0u;
+  h0 = 0x43300000u;
+  k0 += 0x9E3779B9u;
+  k1 += 0xBB67AE85u;
+#pragma unroll
+  for (int r = 1; r < GACT_EXP_ROUNDS; ++r) {
+    uint32_t hi0, hi1, g0, g1;
+    mul_hi_f64<0xD2511F53u>(c0, h0, hi0, g0);
+    mul_hi_f64<0xCD9E8D57u>(c2, h2, hi1, g1);
+    const uint32_t lo0 = c0 * 0xD2511F53u, lo1 = c2 * 0xCD9E8D57u;
+    c0 = xor3(hi1, c1, k0);
+    h0 = g1;
+    c2 = xor3(hi0, c3, k1);
+    h2 = g0;
+    c1 = lo1;
+    c3 = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return make_uint4(c0, c1, c2, c3);
+#else
   uint32_t c0 = (uint32_t)block, c1 = (uint32_t)(block >> 32), c2 = 0u, c3 = 0u;
 #pragma unroll
   for (int r = 0; r < GACT_EXP_ROUNDS; ++r) {
@@ -53,6 +102,7 @@ __device__ __forceinline__ uint4 philox4x32_10(uint64_t block, uint32_t k0, uint
     k1 += 0xBB67AE85u;
   }
   return make_uint4(c0, c1, c2, c3);
+#endif
 }
 
 // ------------------------------------------------------------------- packed f32x2 math
@@ -137,6 +187,12 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p));
   return v;
+}
+
+// Bulk prefetch of [p, p + bytes) into L2 by the TMA unit (one instruction, no registers,
+// no completion tracking). p 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
 // ------------------------------------------------------------- mbarrier / bulk copy (TMA)
