@@ -57,52 +57,56 @@ __device__ __forceinline__ void mul_hi_f64(uint32_t a, uint32_t h, uint32_t& hi,
 #ifndef GACT_EXP_ROUNDS
 #define GACT_EXP_ROUNDS 10  // experiments only: Philox4x32-10 is the defined generator
 #endif
+template <bool F64>
+__device__ __forceinline__ uint4 philox4x32_10_t(uint64_t block, uint32_t k0, uint32_t k1) {
+  if constexpr (F64) {
+    // Round 0 has c2 = c3 = 0 (so M1 c2 = 0); later rounds carry the FP64 high words.
+    uint32_t c1 = (uint32_t)(block >> 32), c3, hi0, h0, h2;
+    const uint32_t a0 = (uint32_t)block;
+    mul_hi_f64<0xD2511F53u>(a0, 0x43300000u, hi0, h2);
+    c3 = a0 * 0xD2511F53u;
+    uint32_t c0 = c1 ^ k0, c2 = hi0 ^ k1;
+    c1 = 0u;
+    h0 = 0x43300000u;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+#pragma unroll
+    for (int r = 1; r < GACT_EXP_ROUNDS; ++r) {
+      uint32_t hi0, hi1, g0, g1;
+      mul_hi_f64<0xD2511F53u>(c0, h0, hi0, g0);
+      mul_hi_f64<0xCD9E8D57u>(c2, h2, hi1, g1);
+      const uint32_t lo0 = c0 * 0xD2511F53u, lo1 = c2 * 0xCD9E8D57u;
+      c0 = xor3(hi1, c1, k0);
+      h0 = g1;
+      c2 = xor3(hi0, c3, k1);
+      h2 = g0;
+      c1 = lo1;
+      c3 = lo0;
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    return make_uint4(c0, c1, c2, c3);
+  } else {
+    uint32_t c0 = (uint32_t)block, c1 = (uint32_t)(block >> 32), c2 = 0u, c3 = 0u;
+#pragma unroll
+    for (int r = 0; r < GACT_EXP_ROUNDS; ++r) {
+      uint32_t lo0, hi0, lo1, hi1;
+      mul_wide(c0, 0xD2511F53u, lo0, hi0);
+      mul_wide(c2, 0xCD9E8D57u, lo1, hi1);
+      const uint32_t n0 = xor3(hi1, c1, k0);
+      const uint32_t n2 = xor3(hi0, c3, k1);
+      c1 = lo1;
+      c3 = lo0;
+      c0 = n0;
+      c2 = n2;
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    return make_uint4(c0, c1, c2, c3);
+  }
+}
 __device__ __forceinline__ uint4 philox4x32_10(uint64_t block, uint32_t k0, uint32_t k1) {
-#if GACT_PHILOX_F64
-  // Round 0 has c2 = c3 = 0 (so M1 c2 = 0); later rounds carry the FP64 high words.
-  uint32_t c1 = (uint32_t)(block >> 32), c3, hi0, h0, h2;
-  const uint32_t a0 = (uint32_t)block;
-  mul_hi_f64<0xD2511F53u>(a0, 0x43300000u, hi0, h2);
-  c3 = a0 * 0xD2511F53u;
-  uint32_t c0 = c1 ^ k0, c2 = hi0 ^ k1;
-  c1 = 0u;
-  h0 = 0x43300000u;
-  k0 += 0x9E3779B9u;
-  k1 += 0xBB67AE85u;
-#pragma unroll
-  for (int r = 1; r < GACT_EXP_ROUNDS; ++r) {
-    uint32_t hi0, hi1, g0, g1;
-    mul_hi_f64<0xD2511F53u>(c0, h0, hi0, g0);
-    mul_hi_f64<0xCD9E8D57u>(c2, h2, hi1, g1);
-    const uint32_t lo0 = c0 * 0xD2511F53u, lo1 = c2 * 0xCD9E8D57u;
-    c0 = xor3(hi1, c1, k0);
-    h0 = g1;
-    c2 = xor3(hi0, c3, k1);
-    h2 = g0;
-    c1 = lo1;
-    c3 = lo0;
-    k0 += 0x9E3779B9u;
-    k1 += 0xBB67AE85u;
-  }
-  return make_uint4(c0, c1, c2, c3);
-#else
-  uint32_t c0 = (uint32_t)block, c1 = (uint32_t)(block >> 32), c2 = 0u, c3 = 0u;
-#pragma unroll
-  for (int r = 0; r < GACT_EXP_ROUNDS; ++r) {
-    uint32_t lo0, hi0, lo1, hi1;
-    mul_wide(c0, 0xD2511F53u, lo0, hi0);
-    mul_wide(c2, 0xCD9E8D57u, lo1, hi1);
-    const uint32_t n0 = xor3(hi1, c1, k0);
-    const uint32_t n2 = xor3(hi0, c3, k1);
-    c1 = lo1;
-    c3 = lo0;
-    c0 = n0;
-    c2 = n2;
-    k0 += 0x9E3779B9u;
-    k1 += 0xBB67AE85u;
-  }
-  return make_uint4(c0, c1, c2, c3);
-#endif
+  return philox4x32_10_t<GACT_PHILOX_F64 != 0>(block, k0, k1);
 }
 
 // ------------------------------------------------------------------- packed f32x2 math
