@@ -46,8 +46,9 @@
  * Conventions for every call
  * ---------------------------------------------------------------------------------
  *  - Ownership: the caller owns and allocates every buffer (PyTorch's caching allocator
- *    in the binding). The library never allocates, frees, synchronises or keeps state;
- *    it is thread-safe. Sizes come from gact_num_groups / gact_packed_words.
+ *    in the binding). The library never allocates, frees, synchronises or keeps state
+ *    (except the staged forms' streams and events, below); it is thread-safe. Sizes come
+ *    from gact_num_groups / gact_packed_words.
  *  - Device calls (x, y, packed, group_min, group_scale are DEVICE pointers) enqueue on
  *    `stream` (a cudaStream_t passed as void*; NULL = legacy default stream) and return
  *    without waiting. gact_allocate_bits takes HOST pointers and runs on the host.
@@ -153,6 +154,35 @@ gact_status gact_quantize_pack_batch(const gact_tensor_desc* descs, int32_t coun
                                      int32_t group_size, void* stream);
 gact_status gact_unpack_dequantize_batch(const gact_tensor_desc* descs, int32_t count,
                                          int32_t group_size, void* stream);
+
+/* Staged (host-buffer) forms — the compressor with its inputs and outputs in HOST memory,
+ * i.e. the paper's "Parallel Swap and Prefetch" (compressed tensors offloaded to
+ * the CPU and swapped back, "two new streams (swap in/out)" ordered by "the CUDA event") as
+ * one call.
+ * Each of data / packed / group_min / group_scale of each descriptor may be a host pointer
+ * (page-locked: the copies overlap the kernels; pageable: correct, copies serialise) or a
+ * device pointer; the library classifies it with cudaPointerGetAttributes. Host buffers
+ * are staged through `workspace` in pieces of whole 4096-element blocks of a tensor:
+ * GACT_STAGED_SLOTS slots of workspace_bytes / GACT_STAGED_SLOTS bytes rotate so that the
+ * host->device copies of piece k+1 (internal stream), the batched kernels of piece k (on
+ * `stream`) and the device->host copies of piece k-1 (second internal stream) overlap;
+ * events order them. The Philox counter of every element stays its index in the whole
+ * tensor, so results are bit-identical to the batch forms on the same descriptors.
+ *   workspace        device, >= GACT_STAGED_MIN_WORKSPACE bytes, 256-byte aligned,
+ *                    caller-owned (contents clobbered)
+ *   stream           work is ordered after everything already enqueued on `stream`
+ * Same validation and alignment rules as the batch forms, plus GACT_ERR_INVALID_ARG for a
+ * NULL / small / misaligned workspace. BLOCKING: returns after every output is written
+ * (host outputs readable, device outputs complete). The internal streams and events are
+ * created once per host thread and device and reused (the only state the library keeps). */
+#define GACT_STAGED_SLOTS 3
+#define GACT_STAGED_MIN_WORKSPACE (3u * 65536u)
+gact_status gact_quantize_pack_staged(const gact_tensor_desc* descs, int32_t count,
+                                      int32_t group_size, void* workspace,
+                                      uint64_t workspace_bytes, void* stream);
+gact_status gact_unpack_dequantize_staged(const gact_tensor_desc* descs, int32_t count,
+                                          int32_t group_size, void* workspace,
+                                          uint64_t workspace_bytes, void* stream);
 
 /* a6 — bit allocation: greedy solution of eqn:ilp (solver P:534)
  *     min_b  sum_l c_l S(b_l)   s.t.  sum_l b_l D_l <= B,   S(b) = (2^b - 1)^-2, S(32) = 0

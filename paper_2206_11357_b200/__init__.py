@@ -26,7 +26,8 @@ __all__ = [
     "lib", "GactError", "F32", "BF16", "F16", "DEFAULT_GROUP", "LADDER",
     "num_groups", "packed_words", "group_stats", "quantize_pack", "unpack_dequantize",
     "quantize_pack_batch", "unpack_dequantize_batch", "allocate_bits", "CompressedTensor",
-    "sq_diff_sum", "S", "BatchPlan",
+    "sq_diff_sum", "S", "BatchPlan", "quantize_pack_staged", "unpack_dequantize_staged",
+    "staged_workspace",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -37,6 +38,9 @@ DEFAULT_GROUP = 256
 LADDER = (1, 2, 4, 8)
 MAX_BATCH = 256
 REDUCE_BLOCKS = 512  # GACT_REDUCE_BLOCKS
+STAGED_SLOTS = 3  # GACT_STAGED_SLOTS
+STAGED_MIN_WORKSPACE = 3 * 65536  # GACT_STAGED_MIN_WORKSPACE
+STAGED_DEFAULT_WORKSPACE = 3 * (64 << 20)
 _TORCH_TAG = {torch.float32: F32, torch.bfloat16: BF16, torch.float16: F16}
 _TAG_TORCH = {v: k for k, v in _TORCH_TAG.items()}
 
@@ -84,6 +88,8 @@ def lib() -> ctypes.CDLL:
             "gact_unpack_dequantize_batch": (i32, [ctypes.POINTER(_Desc), i32, i32, P]),
             "gact_allocate_bits": (i32, [P, P, i32, P, i32, u64, P]),
             "gact_sq_diff_sum": (i32, [P, P, i32, i64, P, P, P]),
+            "gact_quantize_pack_staged": (i32, [ctypes.POINTER(_Desc), i32, i32, P, u64, P]),
+            "gact_unpack_dequantize_staged": (i32, [ctypes.POINTER(_Desc), i32, i32, P, u64, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -131,7 +137,11 @@ class CompressedTensor:
     def nbytes(self) -> int:
         return (self.packed.numel() * 4 + self.group_min.numel() * 4 + self.group_scale.numel() * 4)
 
-    def decompress(self, out: torch.Tensor | None = None) -> torch.Tensor:
+    def decompress(self, out: torch.Tensor | None = None, device=None) -> torch.Tensor:
+        """Device-resident codes: gact_unpack_dequantize. Host-resident codes (a swapped-out
+        context): gact_unpack_dequantize_staged into `out` or a new tensor on `device`."""
+        if not self.packed.is_cuda:
+            return unpack_dequantize_staged([self], None if out is None else [out], device=device)[0]
         return unpack_dequantize(self.packed, self.group_min, self.group_scale, self.numel,
                                  self.bits, self.group_size, self.dtype, out=out).view(self.shape)
 
@@ -225,6 +235,90 @@ def unpack_dequantize_batch(cts: Sequence[CompressedTensor], outs: Sequence[torc
     if rows:
         _check("gact_unpack_dequantize_batch", lib().gact_unpack_dequantize_batch(
             _desc_array(rows), len(rows), gs.pop(), _stream(cts[0].packed)))
+    return ys
+
+
+_workspaces: dict = {}
+
+
+def staged_workspace(device=None, nbytes: int = STAGED_DEFAULT_WORKSPACE) -> torch.Tensor:
+    """The device workspace of the staged calls (cached per device; grows on demand)."""
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    ws = _workspaces.get(dev)
+    if ws is None or ws.numel() < nbytes:
+        ws = _workspaces[dev] = torch.empty(max(nbytes, STAGED_MIN_WORKSPACE), dtype=torch.uint8, device=dev)
+    return ws
+
+
+def _staged_device(tensors, device):
+    if device is not None:
+        return torch.device(device)
+    for t in tensors:
+        if t.is_cuda:
+            return t.device
+    if not torch.cuda.is_available():
+        raise ValueError("libgact runs on CUDA devices only (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _host_out(shape, dtype, like_host: bool, device):
+    if like_host:
+        return torch.empty(shape, dtype=dtype, pin_memory=True)
+    return torch.empty(shape, dtype=dtype, device=device)
+
+
+def quantize_pack_staged(xs: Sequence[torch.Tensor], bits: Sequence[int], seeds: Sequence[int],
+                         group_size: int = DEFAULT_GROUP, outs: Sequence[tuple] | None = None,
+                         device=None, workspace: torch.Tensor | None = None, out_host: bool = True):
+    """Compress tensors that live in HOST memory (pinned for overlap) or on the device, with
+    the compressed context written to host memory (default) or the device: the swap-out of
+    "Parallel Swap and Prefetch" in one blocking libgact call
+    (gact_quantize_pack_staged). Bit-identical to quantize_pack_batch."""
+    dev = _staged_device(xs, device)
+    ws = staged_workspace(dev) if workspace is None else workspace
+    res, rows = [], []
+    for i, (x, b, s) in enumerate(zip(xs, bits, seeds)):
+        if not x.is_contiguous():
+            raise ValueError("quantize_pack_staged needs contiguous tensors")
+        n = x.numel()
+        if outs is None:
+            packed = _host_out(max(packed_words(n, b), 0), torch.int32, out_host, dev)
+            mn = _host_out(max(num_groups(n, group_size), 0), torch.float32, out_host, dev)
+            sc = _host_out(max(num_groups(n, group_size), 0), torch.float32, out_host, dev)
+        else:
+            packed, mn, sc = outs[i]
+        rows.append((x.data_ptr(), packed.data_ptr(), mn.data_ptr(), sc.data_ptr(), n,
+                     s & (2**64 - 1), b, _TORCH_TAG[x.dtype]))
+        res.append(CompressedTensor(packed, mn, sc, tuple(x.shape), x.dtype, b, group_size, s))
+    if rows:
+        with torch.cuda.device(dev):
+            _check("gact_quantize_pack_staged", lib().gact_quantize_pack_staged(
+                _desc_array(rows), len(rows), group_size, ws.data_ptr(), ws.numel(),
+                torch.cuda.current_stream(dev).cuda_stream))
+    return res
+
+
+def unpack_dequantize_staged(cts: Sequence[CompressedTensor], outs: Sequence[torch.Tensor] | None = None,
+                             device=None, workspace: torch.Tensor | None = None, out_host: bool = False):
+    """Decompress contexts whose codes live in HOST memory (or on the device) into device
+    tensors (default; the swap-in + decompress of P:589-592) or host tensors, in one blocking
+    libgact call (gact_unpack_dequantize_staged). Bit-identical to unpack_dequantize_batch."""
+    gs = {c.group_size for c in cts}
+    if len(gs) > 1:
+        raise ValueError("one group size per batch")
+    dev = _staged_device([c.packed for c in cts] + list(outs or []), device)
+    ws = staged_workspace(dev) if workspace is None else workspace
+    ys, rows = [], []
+    for i, c in enumerate(cts):
+        y = _host_out(c.shape, c.dtype, out_host, dev) if outs is None else outs[i]
+        rows.append((y.data_ptr(), c.packed.data_ptr(), c.group_min.data_ptr(),
+                     c.group_scale.data_ptr(), c.numel, 0, c.bits, _TORCH_TAG[y.dtype]))
+        ys.append(y)
+    if rows:
+        with torch.cuda.device(dev):
+            _check("gact_unpack_dequantize_staged", lib().gact_unpack_dequantize_staged(
+                _desc_array(rows), len(rows), gs.pop(), ws.data_ptr(), ws.numel(),
+                torch.cuda.current_stream(dev).cuda_stream))
     return ys
 
 

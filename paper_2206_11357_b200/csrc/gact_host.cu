@@ -66,6 +66,7 @@ QTensor make_q(const void* x, int64_t n, int32_t bits, uint64_t seed, uint32_t* 
   t.n = n;
   t.nwords = ceil_div(n * bits, 32);
   t.seed = seed;
+  t.ctr0 = 0;
   return t;
 }
 
@@ -85,26 +86,88 @@ gact_status from_cuda(cudaError_t e) { return e == cudaSuccess ? GACT_OK : GACT_
 // 16-byte aligned (PyTorch allocations are); otherwise the 16-byte path of the ABI is used.
 bool wide_ok(const void* y, const void* packed) { return aligned(y, 32) && aligned(packed, 16); }
 
-// ----------------------------------------------------------------------- batch helpers
-// Tensors are grouped by (dtype, bits) and each class is launched with one kernel.
-struct ClassKey {
-  int32_t dtype, bits;
-};
+}  // namespace
 
-template <typename Fill>
-gact_status for_each_class(const gact_tensor_desc* d, int32_t count, Fill fill) {
+namespace gact {
+
+// Items are grouped by (dtype, bits); each class is launched in chunks of <= kMaxBatch
+// items, in input order (the parameter blocks are 16 KB: kept off the stack).
+cudaError_t enqueue_quantize(const QItem* items, int32_t count, int log2g, cudaStream_t s) {
+  static thread_local QBatch<kMaxBatch> p;
   bool seen[3][9] = {};
-  for (int32_t i = 0; i < count; ++i) {
-    if (d[i].n == 0) continue;
-    if (seen[d[i].dtype][d[i].bits]) continue;
-    seen[d[i].dtype][d[i].bits] = true;
-    gact_status st = fill(ClassKey{d[i].dtype, d[i].bits});
-    if (st != GACT_OK) return st;
+  for (int32_t c = 0; c < count; ++c) {
+    const int32_t dt = items[c].dtype, bits = items[c].bits;
+    if (items[c].t.n == 0 || seen[dt][bits]) continue;
+    seen[dt][bits] = true;
+    int32_t i = c;
+    while (i < count) {
+      std::memset(&p, 0, offsetof(QBatch<kMaxBatch>, tile_start));
+      p.log2g = log2g;
+      p.Lf = (float)((1 << bits) - 1);
+      int32_t m = 0;
+      int64_t tiles = 0;
+      for (; i < count && m < kMaxBatch; ++i) {
+        const QItem& it = items[i];
+        if (it.t.n == 0 || it.dtype != dt || it.bits != bits) continue;
+        p.tile_start[m] = tiles;
+        p.t[m] = it.t;
+        tiles += quantize_tiles(it.t.n, log2g);
+        ++m;
+      }
+      if (m == 0) break;
+      p.count = m;
+      p.tile_start[m] = tiles;
+      p.tiles_total = tiles;
+      const cudaError_t e = launch_quantize<kMaxBatch>(p, dt, bits, s);
+      if (e != cudaSuccess) return e;
+    }
   }
-  return GACT_OK;
+  return cudaSuccess;
 }
 
-}  // namespace
+cudaError_t enqueue_dequantize(const DItem* items, int32_t count, int log2g, cudaStream_t s) {
+  static thread_local DBatch<kMaxBatch> p;
+  bool seen[3][9] = {};
+  for (int32_t c = 0; c < count; ++c) {
+    const int32_t dt = items[c].dtype, bits = items[c].bits;
+    if (items[c].t.n == 0 || seen[dt][bits]) continue;
+    seen[dt][bits] = true;
+    int32_t i = c;
+    while (i < count) {
+      std::memset(&p, 0, offsetof(DBatch<kMaxBatch>, tile_start));
+      p.log2g = log2g;
+      // the items this launch covers decide the lane width: wide if all are aligned for it
+      int32_t m = 0;
+      bool wide = true;
+      for (int32_t j = i; j < count && m < kMaxBatch; ++j) {
+        const DItem& it = items[j];
+        if (it.t.n == 0 || it.dtype != dt || it.bits != bits) continue;
+        wide = wide && wide_ok(it.t.y, it.t.packed);
+        ++m;
+      }
+      p.lane_elems = wide ? 16 : 8;
+      m = 0;
+      int64_t tiles = 0;
+      for (; i < count && m < kMaxBatch; ++i) {
+        const DItem& it = items[i];
+        if (it.t.n == 0 || it.dtype != dt || it.bits != bits) continue;
+        p.tile_start[m] = tiles;
+        p.t[m] = it.t;
+        tiles += dequant_tiles(it.t.n, p.lane_elems);
+        ++m;
+      }
+      if (m == 0) break;
+      p.count = m;
+      p.tile_start[m] = tiles;
+      p.tiles_total = tiles;
+      const cudaError_t e = launch_dequantize<kMaxBatch>(p, dt, bits, s);
+      if (e != cudaSuccess) return e;
+    }
+  }
+  return cudaSuccess;
+}
+
+}  // namespace gact
 
 // ===================================================================================== ABI
 extern "C" {
@@ -200,34 +263,13 @@ gact_status gact_quantize_pack_batch(const gact_tensor_desc* descs, int32_t coun
     if (st != GACT_OK) return st;
   }
   if (l2 < 0) return GACT_ERR_GROUP_SIZE;
-  static thread_local QBatch<gact::kMaxBatch> p;  // 16 KB: keep it off the stack
-  return for_each_class(descs, count, [&](ClassKey key) -> gact_status {
-    // one launch per <= kMaxBatch tensors of this class, in input order
-    int32_t i = 0;
-    while (i < count) {
-      std::memset(&p, 0, offsetof(QBatch<gact::kMaxBatch>, tile_start));
-      p.log2g = l2;
-      p.Lf = (float)((1 << key.bits) - 1);
-      int32_t m = 0;
-      int64_t tiles = 0;
-      for (; i < count && m < gact::kMaxBatch; ++i) {
-        const gact_tensor_desc& d = descs[i];
-        if (d.n == 0 || d.dtype != key.dtype || d.bits != key.bits) continue;
-        p.tile_start[m] = tiles;
-        p.t[m] = make_q(d.data, d.n, d.bits, d.seed, d.packed, d.group_min, d.group_scale);
-        tiles += gact::quantize_tiles(d.n, l2);
-        ++m;
-      }
-      if (m == 0) break;
-      p.count = m;
-      p.tile_start[m] = tiles;
-      p.tiles_total = tiles;
-      cudaError_t e = gact::launch_quantize<gact::kMaxBatch>(p, key.dtype, key.bits,
-                                                             static_cast<cudaStream_t>(stream));
-      if (e != cudaSuccess) return GACT_ERR_CUDA;
-    }
-    return GACT_OK;
-  });
+  static thread_local std::vector<gact::QItem> items;
+  items.clear();
+  for (int32_t i = 0; i < count; ++i) {
+    const gact_tensor_desc& d = descs[i];
+    items.push_back({make_q(d.data, d.n, d.bits, d.seed, d.packed, d.group_min, d.group_scale), d.dtype, d.bits});
+  }
+  return from_cuda(gact::enqueue_quantize(items.data(), count, l2, static_cast<cudaStream_t>(stream)));
 }
 
 gact_status gact_unpack_dequantize_batch(const gact_tensor_desc* descs, int32_t count,
@@ -240,42 +282,13 @@ gact_status gact_unpack_dequantize_batch(const gact_tensor_desc* descs, int32_t 
     if (st != GACT_OK) return st;
   }
   if (l2 < 0) return GACT_ERR_GROUP_SIZE;
-  static thread_local DBatch<gact::kMaxBatch> p;
-  return for_each_class(descs, count, [&](ClassKey key) -> gact_status {
-    int32_t i = 0;
-    while (i < count) {
-      std::memset(&p, 0, offsetof(DBatch<gact::kMaxBatch>, tile_start));
-      p.log2g = l2;
-      // the chunk of tensors this launch covers decides the lane width: wide if all aligned
-      int32_t m = 0;
-      bool wide = true;
-      for (int32_t j = i; j < count && m < gact::kMaxBatch; ++j) {
-        const gact_tensor_desc& d = descs[j];
-        if (d.n == 0 || d.dtype != key.dtype || d.bits != key.bits) continue;
-        wide = wide && wide_ok(d.data, d.packed);
-        ++m;
-      }
-      p.lane_elems = wide ? 16 : 8;
-      m = 0;
-      int64_t tiles = 0;
-      for (; i < count && m < gact::kMaxBatch; ++i) {
-        const gact_tensor_desc& d = descs[i];
-        if (d.n == 0 || d.dtype != key.dtype || d.bits != key.bits) continue;
-        p.tile_start[m] = tiles;
-        p.t[m] = make_d(d.data, d.n, d.packed, d.group_min, d.group_scale);
-        tiles += gact::dequant_tiles(d.n, p.lane_elems);
-        ++m;
-      }
-      if (m == 0) break;
-      p.count = m;
-      p.tile_start[m] = tiles;
-      p.tiles_total = tiles;
-      cudaError_t e = gact::launch_dequantize<gact::kMaxBatch>(p, key.dtype, key.bits,
-                                                               static_cast<cudaStream_t>(stream));
-      if (e != cudaSuccess) return GACT_ERR_CUDA;
-    }
-    return GACT_OK;
-  });
+  static thread_local std::vector<gact::DItem> items;
+  items.clear();
+  for (int32_t i = 0; i < count; ++i) {
+    const gact_tensor_desc& d = descs[i];
+    items.push_back({make_d(d.data, d.n, d.packed, d.group_min, d.group_scale), d.dtype, d.bits});
+  }
+  return from_cuda(gact::enqueue_dequantize(items.data(), count, l2, static_cast<cudaStream_t>(stream)));
 }
 
 // ------------------------------------------------------------------------- allocator

@@ -17,6 +17,7 @@ struct QTensor {
   int64_t n;
   int64_t nwords;
   uint64_t seed;
+  uint64_t ctr0;  // Philox block counter of x[0]: (element offset of x in its whole tensor) / 8
 };
 
 // Launch parameters (passed by value as __grid_constant__; MAXB = 1 for single calls).
@@ -48,6 +49,21 @@ struct DBatch {
   int64_t tile_start[MAXB + 1];
   DTensor t[MAXB];
 };
+
+// One tensor (or piece of a tensor) of a multi-class enqueue (gact_host.cu).
+struct QItem {
+  QTensor t;
+  int32_t dtype, bits;
+};
+struct DItem {
+  DTensor t;
+  int32_t dtype, bits;
+};
+// Enqueue quantize / dequantize launches for `count` items (any mix of dtypes and bits):
+// one launch per (dtype, bits) class and per <= kMaxBatch items, in input order. Items with
+// n == 0 are skipped. Arguments are assumed validated. Returns the first launch error.
+cudaError_t enqueue_quantize(const QItem* items, int32_t count, int log2g, cudaStream_t s);
+cudaError_t enqueue_dequantize(const DItem* items, int32_t count, int log2g, cudaStream_t s);
 
 // Host-side launchers (gact_quantize.cu / gact_dequant.cu). Return cudaError_t of the launch.
 // `dtype` in {0,1,2}; `bits` in {1,2,4,8}. Tile sizes: quantize max(G, 256), dequant 256.

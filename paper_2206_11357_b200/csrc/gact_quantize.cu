@@ -51,7 +51,7 @@ __device__ __forceinline__ void code_chunk_guarded(const QTensor& T, int64_t e, 
                                                    float inv) {
   float v[8];
   load8_guarded<DT>(v, T.x, e, T.n, mn);
-  const uint4 r = philox4x32_10((uint64_t)e >> 3, (uint32_t)T.seed, (uint32_t)(T.seed >> 32));
+  const uint4 r = philox4x32_10(((uint64_t)e >> 3) + T.ctr0, (uint32_t)T.seed, (uint32_t)(T.seed >> 32));
   store_unit_guarded<BITS>(T.packed, e, T.nwords, quantize_chunk<BITS>(v, mn, inv, r));
 }
 
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
     uint4 rnd[U][CPL];
     if constexpr (!STATS) {
       const uint32_t k0 = (uint32_t)T.seed, k1 = (uint32_t)(T.seed >> 32);
-      const uint64_t blk = (uint64_t)e_lane >> 3;
+      const uint64_t blk = ((uint64_t)e_lane >> 3) + T.ctr0;
 #pragma unroll
       for (int k = 0; k < U; ++k)
 #pragma unroll
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(NW * 32)
           Raw8<DT> raw;
           lds8<DT>(raw, stage + (size_t)(c + i) * kWarpTile * ES);
           const int64_t e = e0 + (c + i) * kWarpTile + lane * kChunk;
-          const uint4 r = philox4x32_10((uint64_t)e >> 3, k0, k1);
+          const uint4 r = philox4x32_10(((uint64_t)e >> 3) + T.ctr0, k0, k1);
           store_unit<BITS>(T.packed, e, quantize_chunk_raw<DT, BITS>(raw, gp.mn, gp.inv, r));
         }
       }
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(kThreads)
     if constexpr (!STATS) {
 #pragma unroll
       for (int k = 0; k < U; ++k)
-        rnd[k] = philox4x32_10(((uint64_t)e_lane >> 3) + k * (kWarpTile / kChunk), (uint32_t)T.seed,
+        rnd[k] = philox4x32_10(((uint64_t)e_lane >> 3) + T.ctr0 + k * (kWarpTile / kChunk), (uint32_t)T.seed,
                                (uint32_t)(T.seed >> 32));
     }
     if (e_warp + U * kWarpTile > T.n) {  // the tensor's last unit: tile by tile, guarded

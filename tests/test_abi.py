@@ -99,6 +99,29 @@ def test_device_call_without_gpu_fails_loudly(L):
         gact.quantize_pack(torch.zeros(256, dtype=torch.bfloat16), 2, 1)
 
 
+def test_staged_validation_and_no_gpu(L):
+    """The staged (host-buffer) forms validate before touching CUDA; with valid arguments
+    and no GPU they fail with GACT_ERR_CUDA (no CPU fallback)."""
+    WS = 0x100000  # 256-byte aligned fake workspace
+    MIN = gact.STAGED_MIN_WORKSPACE
+
+    def call(fn, row, G=256, ws=WS, nbytes=MIN, count=1):
+        return getattr(L, fn)(gact._desc_array([row]), count, G, ws, nbytes, None)
+    ok = (A, A, A, A, 4096, 1, 4, 1)
+    for fn in ("gact_quantize_pack_staged", "gact_unpack_dequantize_staged"):
+        assert call(fn, ok, G=100) == 3
+        assert call(fn, ok[:6] + (3, 1)) == 2
+        assert call(fn, (A + 8,) + ok[1:]) == 4
+        assert call(fn, ok[:1] + (A + 4,) + ok[2:]) == 4
+        assert call(fn, ok[:4] + (-1,) + ok[5:]) == 1
+        assert call(fn, ok, ws=0) == 1
+        assert call(fn, ok, ws=WS + 16) == 1
+        assert call(fn, ok, nbytes=MIN - 1) == 1
+        assert call(fn, ok, count=-1) == 1
+        if not torch.cuda.is_available():
+            assert call(fn, ok) == 6
+
+
 # ---------------------------------------------------------------- host allocator parity
 def test_allocator_matches_oracle(L, orc):
     rng = np.random.default_rng(3)

@@ -1,4 +1,4 @@
 cd /root/repo
-GACT_LIB_PATH=build/var_fb2/libgact.so timeout 600 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -2
-bash tools/gpu_variants_q.sh
-bash tools/gpu_variants_bench.sh
+timeout 900 python -m pytest tests/test_gpu_staged.py -x -q 2>&1 | tail -15
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+timeout 600 python bench.py 2>&1 | tail -1
