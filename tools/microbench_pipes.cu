@@ -48,6 +48,11 @@ __global__ void k(uint32_t* out, uint32_t seed) {
                       asm volatile("fma.rn.f32 %0, %1, %2, %0;" : "+f"(f[c]) : "f"(f[(c+3)%CH]), "f"(f[(c+5)%CH])); } // IMAD + FFMA
       if (OP == 18) { asm volatile("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(f2[c]) : "l"(f2[(c+3)%CH]), "l"(f2[(c+5)%CH])); } // FFMA2 acc chain
       if (OP == 19) { asm volatile("add.rm.f32 %0, %0, 0f4B000000;" : "+f"(f[c])); } // FADD imm
+      if (OP == 20) { asm volatile("add.u32 %0, %0, %1;" : "+r"(a[c]) : "r"(b[c])); } // VIADD / IADD3
+      if (OP == 21) { asm volatile("fma.rm.f64 %0, %0, %1, %2;" : "+l"(f2[c]) : "l"(f2[(c+1)%CH]), "l"(f2[(c+2)%CH])); } // DFMA
+      if (OP == 22) { uint32_t lo, hi; mulw(a[c], 0xD2511F53u, lo, hi); a[c] = lo; b[c] ^= hi;
+                      asm volatile("add.u32 %0, %0, %1;" : "+r"(b[(c+1)%CH]) : "r"(a[(c+3)%CH])); } // IMAD.WIDE + LOP3 + add
+      if (OP == 23) { asm volatile("mov.u32 %0, %1;" : "=r"(a[c]) : "r"(b[(c+1)%CH])); asm volatile("xor.b32 %0, %0, %1;" : "+r"(b[c]) : "r"(a[c])); } // MOV + LOP3
     }
   }
   uint32_t s = 0;
@@ -81,5 +86,6 @@ int main() {
   run<11>("FFMA acc", 1); run<12>("IMADW+LOP3+2FFMA", 4); run<13>("IMADW+LOP3+FFMA2", 3);
   run<14>("IMADW+LOP3+FADD2", 3); run<15>("FHADD.BF16 (sub)", 1); run<16>("HMNMX2.BF16", 1);
   run<17>("IMAD+FFMA", 2); run<18>("FFMA2 acc", 1); run<19>("FADD imm", 1);
+  run<20>("IADD (add.u32)", 1); run<21>("DFMA", 1); run<22>("IMADW+LOP3+add", 3); run<23>("MOV+LOP3", 2);
   return 0;
 }
