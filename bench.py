@@ -412,7 +412,21 @@ def cpu_baseline(xs, specs, G, budget_s, avg_bits, dtype):
     return {"value": round(nbytes / secs / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
             "sample": f"first {64 * G} elements of each of the {len(xs)} tensors at b={bits}, "
                       f"cycled for {secs:.1f} s ({elems} elements quantized+dequantized)",
-            "cpu": _cpu_model()}
+            "cpu": _cpu_model(), "all_cores": oracle_all_cores(samples, G, bits, budget_s / 2)}
+
+
+def oracle_all_cores(samples, G, bits, budget_s):
+    """The same oracle and sample with the tensors partitioned over every host core (one
+    thread each: ctypes releases the GIL during the C calls)."""
+    from concurrent.futures import ThreadPoolExecutor
+    n = max(1, min(os.cpu_count() or 1, len(samples)))
+    parts = [samples[i::n] for i in range(n)]
+    with ThreadPoolExecutor(n) as ex:
+        res = list(ex.map(lambda part: oracle_sample_pass(part, G, lambda i: bits, budget_s), parts))
+    nbytes = sum(r[0] for r in res)
+    secs = max(r[1] for r in res)
+    return {"value": round(nbytes / secs / 1e9, 4), "unit": "GB/s", "cores": n,
+            "sample": f"the same sample, tensors partitioned over {n} threads, {secs:.1f} s"}
 
 
 def _cpu_model():
