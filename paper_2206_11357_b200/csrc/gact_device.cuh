@@ -479,6 +479,51 @@ __device__ __forceinline__ void chunk_minmax_raw(const Raw8<DT>& raw, float& mn,
   }
 }
 
+template <int DT>
+__device__ __forceinline__ uint32_t min2_packed(uint32_t a, uint32_t b) {
+  uint32_t r;
+  if constexpr (DT == DT_BF16) asm("min.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  else asm("min.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+// 2-byte dtypes: the chunk's (min, -max) as one packed pair (low half: min, high half: the
+// negated max), so that a segmented butterfly moves and reduces both with one shuffle and one
+// 2-wide min (HMNMX2) per step. Exact: negation flips the sign bit, and min / max of bf16 /
+// f16 values equal those of their (exact) binary32 widenings.
+template <int DT>
+__device__ __forceinline__ uint32_t chunk_minnegmax_packed(const Raw8<DT>& raw) {
+  static_assert(DT != DT_F32, "2-byte dtypes only");
+  uint32_t m01, m23, m, M01, M23, M;
+  if constexpr (DT == DT_BF16) {
+    asm("min.bf16x2 %0, %1, %2;" : "=r"(m01) : "r"(raw.a.x), "r"(raw.a.y));
+    asm("min.bf16x2 %0, %1, %2;" : "=r"(m23) : "r"(raw.a.z), "r"(raw.a.w));
+    asm("min.bf16x2 %0, %1, %2;" : "=r"(m) : "r"(m01), "r"(m23));
+    asm("max.bf16x2 %0, %1, %2;" : "=r"(M01) : "r"(raw.a.x), "r"(raw.a.y));
+    asm("max.bf16x2 %0, %1, %2;" : "=r"(M23) : "r"(raw.a.z), "r"(raw.a.w));
+    asm("max.bf16x2 %0, %1, %2;" : "=r"(M) : "r"(M01), "r"(M23));
+  } else {
+    asm("min.f16x2 %0, %1, %2;" : "=r"(m01) : "r"(raw.a.x), "r"(raw.a.y));
+    asm("min.f16x2 %0, %1, %2;" : "=r"(m23) : "r"(raw.a.z), "r"(raw.a.w));
+    asm("min.f16x2 %0, %1, %2;" : "=r"(m) : "r"(m01), "r"(m23));
+    asm("max.f16x2 %0, %1, %2;" : "=r"(M01) : "r"(raw.a.x), "r"(raw.a.y));
+    asm("max.f16x2 %0, %1, %2;" : "=r"(M23) : "r"(raw.a.z), "r"(raw.a.w));
+    asm("max.f16x2 %0, %1, %2;" : "=r"(M) : "r"(M01), "r"(M23));
+  }
+  const uint32_t nM = M ^ 0x80008000u;
+  return min2_packed<DT>(__byte_perm(m, nM, 0x5410), __byte_perm(m, nM, 0x7632));
+}
+// (min, -max) pair -> binary32 (mn, mx).
+template <int DT>
+__device__ __forceinline__ void unpack_minmax(uint32_t p, float& mn, float& mx) {
+  if constexpr (DT == DT_BF16) {
+    mn = __uint_as_float(p << 16);
+    mx = __uint_as_float((p & 0xFFFF0000u) ^ 0x80000000u);
+  } else {
+    mn = f16_bits_to_f32(p & 0xFFFFu);
+    mx = f16_bits_to_f32((p >> 16) ^ 0x8000u);
+  }
+}
+
 // Store the chunk's packed unit at byte address p. Element e0 (multiple of 8) starts at
 // bit e0*BITS, a byte boundary; the unit is 8*BITS bits: u8 / u16 / u32 / u64.
 template <int BITS>

@@ -96,6 +96,9 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 #ifndef GACT_Q_WAVES
 #define GACT_Q_WAVES 8
 #endif
+#ifndef GACT_QS_MINB
+#define GACT_QS_MINB 3  // small-G kernel: minimum resident CTAs per SM (register cap)
+#endif
 #ifndef GACT_Q_PREFETCH
 #define GACT_Q_PREFETCH 0
 #endif
@@ -295,13 +298,13 @@ __device__ __forceinline__ void small_tile(const QTensor& T, int64_t e, bool ful
   }
 }
 
-template <int DT, int BITS, int MAXB, bool STATS>
-__global__ void __launch_bounds__(kThreads)
+template <int DT, int BITS, int MAXB, bool STATS, int LOG2G>
+__global__ void __launch_bounds__(kThreads, GACT_QS_MINB)
     quantize_small_kernel(const __grid_constant__ QBatch<MAXB> P) {
   constexpr int U = 4;
   const int lane = threadIdx.x & 31;
   const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
-  const int lpg = 1 << (P.log2g - 3);  // lanes per group
+  constexpr int lpg = 1 << (LOG2G - 3);  // lanes per group
   const int warp = threadIdx.x >> 5;
   constexpr int CU = kWarps * U;
   int cur = 0;
@@ -337,14 +340,22 @@ __global__ void __launch_bounds__(kThreads)
     float mnk[U], mxk[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      float lmn = FLT_MAX, lmx = -FLT_MAX;
-      chunk_minmax_raw<DT>(raw[k], lmn, lmx);
-      for (int o = 1; o < lpg; o <<= 1) {
-        lmn = fminf(lmn, __shfl_xor_sync(kFull, lmn, o));
-        lmx = fmaxf(lmx, __shfl_xor_sync(kFull, lmx, o));
+      if constexpr (DT == DT_F32) {
+        float lmn = FLT_MAX, lmx = -FLT_MAX;
+        chunk_minmax_raw<DT>(raw[k], lmn, lmx);
+#pragma unroll
+        for (int o = 1; o < lpg; o <<= 1) {
+          lmn = fminf(lmn, __shfl_xor_sync(kFull, lmn, o));
+          lmx = fmaxf(lmx, __shfl_xor_sync(kFull, lmx, o));
+        }
+        mnk[k] = lmn;
+        mxk[k] = lmx;
+      } else {  // (min, -max) packed in one register: one shuffle + one HMNMX2 per step
+        uint32_t pm = chunk_minnegmax_packed<DT>(raw[k]);
+#pragma unroll
+        for (int o = 1; o < lpg; o <<= 1) pm = min2_packed<DT>(pm, __shfl_xor_sync(kFull, pm, o));
+        unpack_minmax<DT>(pm, mnk[k], mxk[k]);
       }
-      mnk[k] = lmn;
-      mxk[k] = lmx;
     }
     const int sl = lane & (lpg - 1);  // lane within its group's segment
     const int sel = sl & (U - 1);
@@ -429,8 +440,12 @@ template <int DT, int BITS, int MAXB, bool STATS>
 cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
   const int waves = DT == DT_F32 ? 1 : GACT_Q_WAVES;
   switch (p.log2g) {
-    case 5: case 6: case 7:
-      return launch_persistent<quantize_small_kernel<DT, BITS, MAXB, STATS>>(p, 4, s, waves);
+    case 5:
+      return launch_persistent<quantize_small_kernel<DT, BITS, MAXB, STATS, 5>>(p, 4, s, waves);
+    case 6:
+      return launch_persistent<quantize_small_kernel<DT, BITS, MAXB, STATS, 6>>(p, 4, s, waves);
+    case 7:
+      return launch_persistent<quantize_small_kernel<DT, BITS, MAXB, STATS, 7>>(p, 4, s, waves);
     case 8:
       return launch_persistent<quantize_big_kernel<DT, BITS, 1, MAXB, STATS>>(p, kQuantUnit, s, waves);
     case 9:
