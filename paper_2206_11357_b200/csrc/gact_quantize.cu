@@ -203,7 +203,8 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
 }
 
 // ---------------------------------------------------------------------------------------
-// G in {2048, 4096}: the group does not fit in registers. Pass 1 streams it from HBM once,
+// G in {2048, 4096}, 2-byte inputs: the group does not fit in one warp's registers. Pass 1
+// streams it from HBM once,
 // folding min/max and parking each lane's chunks in shared memory (G * s_in bytes per warp,
 // each lane re-reads only what it wrote: no synchronisation); pass 2 codes from shared memory.
 template <int DT, int BITS, int MAXB, bool STATS, int NW>
@@ -256,6 +257,94 @@ __global__ void __launch_bounds__(NW * 32)
           const uint4 r = philox4x32_10(((uint64_t)e >> 3) + T.ctr0, k0, k1);
           store_unit<BITS>(T.packed, e, quantize_chunk_raw<DT, BITS>(raw, gp.mn, gp.inv, r));
         }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// G in {2048, 4096}, fp32 inputs: a group spans the CTA (8 warps x CPW chunks per lane), all in
+// registers; U = 4/CPW groups per CTA unit. Per group each warp reduces its share with
+// CREDUX, parks it in shared memory (double-buffered by unit parity: one barrier per unit),
+// and re-reduces the 8 warp partials with CREDUX; the U divisions run on U lanes.
+template <int DT, int BITS, int CPW, int MAXB, bool STATS>
+__global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
+    quantize_cta_kernel(const __grid_constant__ QBatch<MAXB> P) {
+  constexpr int U = 4 / CPW;                  // groups per CTA unit
+  constexpr int WE = CPW * kWarpTile;         // elements of a group per warp
+  constexpr int TE = kWarps * WE;             // == G
+  __shared__ float red[2][U][2][kWarps];      // [parity][group][min, max][warp]
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
+  const int64_t cunits = P.tiles_total / U;   // a quantize tile is one group here
+  int cur = 0, par = 0;
+  for (int64_t cu = blockIdx.x; cu < cunits; cu += gridDim.x, par ^= 1) {
+    cur = advance_cursor(P, cur, cu * U);
+    const QTensor& T = P.t[cur];
+    const int64_t e_unit = (cu * U - P.tile_start[cur]) * TE;
+    if (e_unit + U * TE > T.n) {  // CTA-uniform: the tensor's last unit, warp k codes group k
+      if (warp < U && e_unit + warp * TE < T.n)
+        tile_generic<DT, BITS, STATS>(T, e_unit + warp * TE, P.log2g, Lf, lane);
+      continue;
+    }
+    const int64_t e_lane = e_unit + warp * WE + lane * kChunk;
+    Raw8<DT> raw[U][CPW];
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) load8<DT>(raw[k][c], T.x, e_lane + k * TE + c * kWarpTile);
+    uint4 rnd[U][CPW];
+    if constexpr (!STATS) {
+      const uint32_t k0 = (uint32_t)T.seed, k1 = (uint32_t)(T.seed >> 32);
+      const uint64_t blk = ((uint64_t)e_lane >> 3) + T.ctr0;
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+#pragma unroll
+        for (int c = 0; c < CPW; ++c) rnd[k][c] = philox4x32_10(blk + (k * TE + c * kWarpTile) / kChunk, k0, k1);
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      float lmn = FLT_MAX, lmx = -FLT_MAX;
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) chunk_minmax_raw<DT>(raw[k][c], lmn, lmx);
+      lmn = warp_min(lmn);
+      lmx = warp_max(lmx);
+      if (lane == 0) {
+        red[par][k][0][warp] = lmn;
+        red[par][k][1][warp] = lmx;
+      }
+    }
+    __syncthreads();
+    float mnk[U], mxk[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      mnk[k] = warp_min(red[par][k][0][lane & (kWarps - 1)]);
+      mxk[k] = warp_max(red[par][k][1][lane & (kWarps - 1)]);
+    }
+    const int sel = lane & (U - 1);
+    float a = mnk[0], b = mxk[0];
+#pragma unroll
+    for (int k = 1; k < U; ++k) {
+      a = (sel == k) ? mnk[k] : a;
+      b = (sel == k) ? mxk[k] : b;
+    }
+    const GroupParams gp = group_params(a, b, Lf);
+    if (warp == 0 && lane < U) {
+      const int64_t g = (e_unit >> P.log2g) + lane;
+      T.group_min[g] = gp.mn;
+      T.group_scale[g] = gp.scale;
+    }
+    if constexpr (!STATS) {
+      unsigned char* out = reinterpret_cast<unsigned char*>(T.packed) + (e_lane * BITS) / 8;
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const float inv = __shfl_sync(kFull, gp.inv, k);
+        const float mn = __fadd_rn(mnk[k], 0.0f);
+#pragma unroll
+        for (int c = 0; c < CPW; ++c)
+          store_unit_at<BITS>(out + ((k * TE + c * kWarpTile) * BITS) / 8,
+                              quantize_chunk_raw<DT, BITS>(raw[k][c], mn, inv, rnd[k][c]));
       }
     }
   }
@@ -409,6 +498,17 @@ cudaError_t launch_persistent(const PB& p, int64_t tiles_per_warp_iter, cudaStre
   return cudaGetLastError();
 }
 
+// One CTA per unit of `tiles_per_unit` tiles, up to `waves` x resident CTAs.
+template <auto Kernel, typename PB>
+cudaError_t launch_units(const PB& p, int64_t tiles_per_unit, cudaStream_t s, int waves = 1) {
+  static const int per_sm = max_blocks_per_sm(Kernel);
+  const int64_t want = (p.tiles_total + tiles_per_unit - 1) / tiles_per_unit;
+  const int64_t cap = (int64_t)sm_count() * per_sm * waves;
+  const int grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
+  Kernel<<<grid, kThreads, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
 template <int DT, int BITS, int MAXB, bool STATS, int NW>
 cudaError_t launch_staged_nw(const QBatch<MAXB>& p, int smem, cudaStream_t s) {
   constexpr auto kernel = quantize_staged_kernel<DT, BITS, MAXB, STATS, NW>;
@@ -453,7 +553,14 @@ cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
     case 10:
       return launch_persistent<quantize_big_kernel<DT, BITS, 4, MAXB, STATS>>(p, kQuantUnit > 4 ? kQuantUnit / 4 : 1, s, waves);
     default:
-      return launch_staged<DT, BITS, MAXB, STATS>(p, s);
+      // fp32 (HBM-bound): the group spread over the CTA in registers (+10-24%); 2-byte inputs
+      // (FMA-bound): the per-warp shared-memory stage, which needs no CTA barrier.
+      if constexpr (DT == DT_F32) {
+        if (p.log2g == 11) return launch_units<quantize_cta_kernel<DT, BITS, 1, MAXB, STATS>>(p, 4, s, waves);
+        return launch_units<quantize_cta_kernel<DT, BITS, 2, MAXB, STATS>>(p, 2, s, waves);
+      } else {
+        return launch_staged<DT, BITS, MAXB, STATS>(p, s);
+      }
   }
 }
 
