@@ -24,12 +24,15 @@
  *     inv   = range == 0 ? 0 : L / range                        (round toward ZERO)
  * and for every element i of the group
  *     d_i = x_i - mn                                             (round to nearest)
- *     t_i = fma(d_i, inv, 2^-17)                                 (one rounding, nearest)
- *     q_i = floor(t_i + k_i 2^-16),  k_i = 16-bit Philox lane of (seed, i)  (below)
- *                                     (exact real floor; 0 < t_i <= L + 2^-17, q_i in [0, L])
+ *     T_i = d_i * inv                                            (EXACT real product)
+ *     q_i = floor(T_i + (2 k_i + 1) 2^-17),  k_i = 16-bit Philox lane of (seed, i)  (below)
+ *                                     (exact real floor, no rounding of T_i; q_i in [0, L]
+ *                                      because T_i <= range * RZ(L / range) <= L)
  * which is T_{h,b} of P:233 followed by the stochastic rounding of P:229-230:
- * q_i = ceil(T) with probability frac(T) (up to 2^-17: the 2^-17 offset centres the
- * 2^-16 lattice of thresholds), else floor(T).
+ * q_i = ceil(T) with probability frac(T) (up to 2^-17: u = (2k+1) 2^-17 is the centred
+ * 2^-16 lattice of thresholds), else floor(T); q_i = T_i when T_i is an integer.
+ * (R2, R4, R5; the GPU evaluates it exactly as fma.rm(d, inv, 64 + u) followed
+ * by add.rm(., 2^23 - 64), the oracle as floor(P) + [P - floor(P) >= 1 - u] in binary64.)
  * Decompression (T^{-1}):   y_i = fma(q_i, scale, mn) in binary32, then
  * rounded to nearest-even into the output dtype.
  *
