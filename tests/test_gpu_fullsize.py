@@ -132,3 +132,28 @@ def test_bert_layer(gact, orc):
 
 def test_gcn_swin_rank1(gact, orc):
     _run_workload(gact, orc, "gcn_swin", 2.0, rank=1)
+
+
+def test_bert_layer_staged_host_buffers(gact, orc):
+    """The host-buffer forms (the bench's e2e path) at full size: one BERT-large layer
+    (2^30 elements, 2 GiB bf16) from pinned host memory through the default workspace,
+    bit-identical to the device batch forms everywhere, and oracle-exact on sampled groups."""
+    specs = synth.workload_specs("bert_layer")
+    xs = [synth.make_tensor(s, synth.DATA_SEED + i, "cuda", torch.bfloat16) for i, s in enumerate(specs)]
+    D = np.array([s.numel for s in specs], dtype=np.int64)
+    bits = gact.allocate_bits(synth.sensitivities(specs, seed=7), D, int(2.0 * D.sum())).tolist()
+    seeds = [synth.tensor_seed(2022, i) for i in range(len(specs))]
+    ref = gact.quantize_pack_batch(xs, bits, seeds, G)
+    hx = [x.cpu().pin_memory() for x in xs]
+    got = gact.quantize_pack_staged(hx, bits, seeds, G)
+    for a, b in zip(got, ref):
+        assert not a.packed.is_cuda
+        for ha, db in ((a.packed, b.packed), (a.group_min, b.group_min), (a.group_scale, b.group_scale)):
+            assert torch.equal(ha.cuda().view(torch.int32), db.view(torch.int32))
+    ys = gact.unpack_dequantize_staged(got)
+    ys_ref = gact.unpack_dequantize_batch(ref)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(5)
+    for x, ct, y, yr, b, s in zip(xs, got, ys, ys_ref, bits, seeds):
+        assert torch.equal(y.view(torch.int16), yr.view(torch.int16))
+        _check_sampled(orc, x, ct, y, int(b), s, rng, nsamples=3)
