@@ -99,6 +99,9 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 #ifndef GACT_QS_MINB
 #define GACT_QS_MINB 3  // small-G kernel: minimum resident CTAs per SM (register cap)
 #endif
+#ifndef GACT_Q_RNG_EARLY
+#define GACT_Q_RNG_EARLY 64  // Philox blocks per lane computed while the unit's loads fly
+#endif
 #ifndef GACT_Q_PREFETCH
 #define GACT_Q_PREFETCH 0
 #endif
@@ -155,14 +158,15 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
     // iteration ahead, or in separate producer warps fed by TMA bulk copies, were both
     // measured slower on B200: DESIGN.md §4.)
     uint4 rnd[U][CPL];
+    const uint32_t k0 = (uint32_t)T.seed, k1 = (uint32_t)(T.seed >> 32);
+    const uint64_t blk = ((uint64_t)e_lane >> 3) + T.ctr0;
     if constexpr (!STATS) {
-      const uint32_t k0 = (uint32_t)T.seed, k1 = (uint32_t)(T.seed >> 32);
-      const uint64_t blk = ((uint64_t)e_lane >> 3) + T.ctr0;
 #pragma unroll
       for (int k = 0; k < U; ++k)
 #pragma unroll
         for (int c = 0; c < CPL; ++c)
-          rnd[k][c] = philox4x32_10(blk + (k * TE + c * kWarpTile) / kChunk, k0, k1);
+          if (k * CPL + c < GACT_Q_RNG_EARLY)
+            rnd[k][c] = philox4x32_10(blk + (k * TE + c * kWarpTile) / kChunk, k0, k1);
     }
     float mnk[U], mxk[U];
 #pragma unroll
@@ -194,9 +198,12 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
         const float inv = __shfl_sync(kFull, gp.inv, k);
         const float mn = __fadd_rn(mnk[k], 0.0f);
 #pragma unroll
-        for (int c = 0; c < CPL; ++c)
+        for (int c = 0; c < CPL; ++c) {
+          if (k * CPL + c >= GACT_Q_RNG_EARLY)  // late blocks: computed just before use
+            rnd[k][c] = philox4x32_10(blk + (k * TE + c * kWarpTile) / kChunk, k0, k1);
           store_unit_at<BITS>(out + ((k * TE + c * kWarpTile) * BITS) / 8,
                               quantize_chunk_raw<DT, BITS>(raw[k][c], mn, inv, rnd[k][c]));
+        }
       }
     }
   }
