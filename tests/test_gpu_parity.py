@@ -125,7 +125,9 @@ def test_c1_config(gact, orc):
 @pytest.mark.parametrize("G", GROUPS)
 def test_quantize_dequantize_parity(gact, orc, dtype, bits, G):
     TE = max(G, 256)
-    n = 3 * TE + 8 * 5 + 3  # several tiles, a ragged tail, a partial chunk
+    # two full CTA units (8192 elements: the unguarded fast path of every kernel), then
+    # several tiles, a ragged tail and a partial chunk (the guarded path)
+    n = 2 * 8192 + 3 * TE + 8 * 5 + 3
     x = make_input(n, dtype, seed=G * 10 + bits)
     ct, ref = check_quantize(gact, orc, x, G, bits, seed=0xABCDEF0123456789 ^ (G * bits))
     for ydt in DTYPES:
