@@ -41,7 +41,7 @@ def _same(ct_a, ct_b):
         assert np.array_equal(host_bits(a), host_bits(b))
 
 
-@pytest.mark.parametrize("G", [32, 256, 4096])
+@pytest.mark.parametrize("G", [32, 256, 2048, 4096])
 @pytest.mark.parametrize("ws_bytes", [3 * 65536, 3 * (1 << 20), 3 * (64 << 20)])
 def test_staged_quantize_equals_batch(gact, G, ws_bytes):
     xs, bits, seeds = _inputs()
