@@ -32,7 +32,10 @@
  * q_i = ceil(T) with probability frac(T) (up to 2^-17: u = (2k+1) 2^-17 is the centred
  * 2^-16 lattice of thresholds), else floor(T); q_i = T_i when T_i is an integer.
  * (R2, R4, R5; the GPU evaluates it exactly as fma.rm(d, inv, 64 + u) followed
- * by add.rm(., 2^23 - 64), the oracle as floor(P) + [P - floor(P) >= 1 - u] in binary64.)
+ * by add.rm(., 2^23 - 64) for b = 8, and as fma.rn(d, inv, 128 + k 2^-16) -- round to
+ * nearest on the 2^-16 grid of [128, 256), which adds the 2^-17 half-step -- followed by
+ * add.rm(., 2^23 - 128) for b <= 4; the oracle as floor(P) + [P - floor(P) >= 1 - u] in
+ * binary64.)
  * Decompression (T^{-1}):   y_i = fma(q_i, scale, mn) in binary32, then
  * rounded to nearest-even into the output dtype.
  *

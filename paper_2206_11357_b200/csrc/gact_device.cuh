@@ -364,21 +364,40 @@ __device__ __forceinline__ constexpr uint32_t magic_sum(int first, int count) {
 // c = 64 + (2k+1) 2^-17: PRMT builds 0x4300_0000 | k = 128 + k 2^-16, then one exact FADD2
 // adds 2^-17 - 64. (Building c in the integer pipe instead -- funnel shift + lop3 -- was
 // measured slower: it overloads the ALU pipe that the Philox xors and byte permutes use.)
+//
+// b <= 4 (L <= 15) needs one instruction fewer, with bit-identical codes: with
+// c' = 128 + k 2^-16 (the PRMT result itself) every X = d*inv + c' lies in the binade
+// [128, 256), whose spacing is 2^-16, so v' = fma.rn(d, inv, c') rounds X to the nearest
+// multiple of 2^-16. v' reaches the next integer N exactly when X >= N - 2^-17 (the tie
+// X = N - 2^-17 goes to the even neighbour, N itself, as N 2^16 is even), hence
+// floor(v') = floor(X + 2^-17) = 128 + floor(T + (2k+1) 2^-17) = 128 + q. X <= 128 + L +
+// 1 - 2^-16 keeps v' below 128 + L + 1 < 256 (no binade change), and add.rm(v', 2^23 - 128)
+// gives bits 0x4B00_0000 + q as before. b = 8 (v up to 384) would cross into [256, 512),
+// spacing 2^-15, so it keeps the exact fma.rm form above.
+template <int BITS>
 __device__ __forceinline__ void code_pair(f2_t d2, f2_t inv2, uint32_t rw, uint32_t& w_lo,
                                           uint32_t& w_hi) {
-  const f2_t cofs = f2_make(0x1p-17f - 64.0f, 0x1p-17f - 64.0f);
-  const f2_t magic = f2_make(8388608.0f - 64.0f, 8388608.0f - 64.0f);
   const uint32_t klo = __byte_perm(rw, 0x43000000u, 0x7610);  // 128 + k_lo 2^-16
   const uint32_t khi = __byte_perm(rw, 0x43000000u, 0x7632);  // 128 + k_hi 2^-16
-  const f2_t c2 = f2_add_rn(f2_bits(klo, khi), cofs);
-  const f2_t w2 = f2_add_rm(f2_fma_rm(d2, inv2, c2), magic);
+  f2_t w2;
+  if constexpr (BITS <= 4) {
+    const f2_t magic = f2_make(8388608.0f - 128.0f, 8388608.0f - 128.0f);
+    w2 = f2_add_rm(f2_fma_rn(d2, inv2, f2_bits(klo, khi)), magic);
+  } else {
+    const f2_t cofs = f2_make(0x1p-17f - 64.0f, 0x1p-17f - 64.0f);
+    const f2_t magic = f2_make(8388608.0f - 64.0f, 8388608.0f - 64.0f);
+    const f2_t c2 = f2_add_rn(f2_bits(klo, khi), cofs);
+    w2 = f2_add_rm(f2_fma_rm(d2, inv2, c2), magic);
+  }
   f2_split_bits(w2, w_lo, w_hi);
 }
 
 // Pack the low bytes q_j of w_j (= 0x4B00_0000 + q_j) into the chunk's 8*BITS-bit unit:
 // b = 8 by byte permutes; b < 8 by one IMAD per code (acc + (w_j << b j), mod 2^32), minus
-// the constant sum of the 0x4B00_0000 terms. (A byte-permute + funnel-shift packing that
-// keeps b < 8 in the integer pipe was measured slower: that pipe is as busy as the FMA pipe.)
+// the constant sum of the 0x4B00_0000 terms. Integer-pipe alternatives were measured slower
+// or equal (2^28 bf16): gathering the even / odd low bytes with 6 PRMT and
+// merging them (b = 1: 177 vs 166 us, b = 2: 183 vs 166, b = 4: 172 vs 167), and pairwise
+// IMAD + 3 PRMT (169 / 168 / 166): the integer pipe is as busy as the FMA-heavy pipe.
 template <int BITS>
 __device__ __forceinline__ PackedUnit<BITS> pack_codes(const uint32_t w[8]) {
   PackedUnit<BITS> out;
@@ -404,7 +423,7 @@ __device__ __forceinline__ PackedUnit<BITS> quantize_chunk(const float v[8], flo
   uint32_t w[8];
 #pragma unroll
   for (int p = 0; p < 4; ++p)
-    code_pair(f2_sub_rn(f2_make(v[2 * p], v[2 * p + 1]), mn2), inv2, words[p], w[2 * p], w[2 * p + 1]);
+    code_pair<BITS>(f2_sub_rn(f2_make(v[2 * p], v[2 * p + 1]), mn2), inv2, words[p], w[2 * p], w[2 * p + 1]);
   return pack_codes<BITS>(w);
 }
 
@@ -440,7 +459,7 @@ __device__ __forceinline__ PackedUnit<BITS> quantize_chunk_raw(const Raw8<DT>& r
             "sub.rn.f32.f16 %1, h, %3;\n\t}"
             : "=f"(dlo), "=f"(dhi) : "r"(xw[p]), "f"(mn));
       }
-      code_pair(f2_make(dlo, dhi), inv2, words[p], w[2 * p], w[2 * p + 1]);
+      code_pair<BITS>(f2_make(dlo, dhi), inv2, words[p], w[2 * p], w[2 * p + 1]);
     }
     return pack_codes<BITS>(w);
   }
