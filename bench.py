@@ -37,7 +37,7 @@ WORKLOAD_CONFIG = {
     "bert_layer": "BERT-large seq 512 batch 64, one layer (12 tensors), avg 2 bits [configs[3]]",
     "bert24": "BERT-large seq 512 batch 64, 24 layers, avg 2 bits [configs[3]]",
     "gcn_swin": "GCN ogbn-arxiv-shaped + Swin-T batch 128 per rank, avg 2 bits [configs[4]]",
-    "buf256": "256 MiB bf16 buffer, b=2 [configs[1]]",
+    "buf256": "256 MiB bf16 buffer, b = avg_bits_budget (default 2) [configs[1]]",
 }
 
 

@@ -93,6 +93,9 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 // Grid = waves x resident CTAs. Several waves (CTAs pick up units dynamically as others
 // retire) beat a persistent grid for the FMA-bound 2-byte inputs (+6% at bf16); fp32 inputs
 // (HBM-bound) keep the persistent grid. Measured on B200: DESIGN.md §4.
+#ifndef GACT_Q_WAVES_F32
+#define GACT_Q_WAVES_F32 1
+#endif
 #ifndef GACT_Q_WAVES
 #define GACT_Q_WAVES 8
 #endif
@@ -545,7 +548,7 @@ cudaError_t launch_staged(const QBatch<MAXB>& p, cudaStream_t s) {
 
 template <int DT, int BITS, int MAXB, bool STATS>
 cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
-  const int waves = DT == DT_F32 ? 1 : GACT_Q_WAVES;
+  const int waves = DT == DT_F32 ? GACT_Q_WAVES_F32 : GACT_Q_WAVES;
   switch (p.log2g) {
     case 5:
       return launch_persistent<quantize_small_kernel<DT, BITS, MAXB, STATS, 5>>(p, 4, s, waves);

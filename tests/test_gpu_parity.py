@@ -288,3 +288,22 @@ def test_dequant_narrow_and_wide_paths_agree(gact, bits):
                                         out=ybuf[pad:])
         torch.cuda.synchronize()
         assert torch.equal(narrow, wide)
+
+
+@pytest.mark.parametrize("bits", BITS)
+@pytest.mark.parametrize("G", [32, 256, 1024])
+def test_threshold_ties(gact, orc, bits, G):
+    """T + u exactly on an integer and one fp32 step either side (tests/tie_cases.py): the
+    GPU's rounding shortcuts for the exact floor(T + u) (fma.rm for b = 8, fma.rn on the
+    2^-16 grid for b <= 4; R5) agree with the oracle and the closed form, on the
+    unguarded fast path (>= 2 CTA units) and a ragged tail."""
+    import tie_cases
+    seed = 0x5EED0000 + G * 16 + bits
+    ng = max(2 * 8192 // G, 2) + 3
+    xh, want = tie_cases.tie_groups(ng, G, bits, seed, orc.lane16, np.random.default_rng(G + bits))
+    xh = xh[: xh.size - 5]  # ragged tail: the last group is short
+    want = want[: xh.size]
+    x = torch.from_numpy(xh).cuda()
+    ct, ref = check_quantize(gact, orc, x, G, bits, seed)
+    q = orc.unpack(host_bits(ct.packed), xh.size, bits).astype(np.int64)
+    assert np.array_equal(q, want)

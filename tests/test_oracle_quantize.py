@@ -251,3 +251,19 @@ def test_tiny_and_subnormal_ranges(orc):
         assert np.array_equal(y[:256], x[:256])
         assert np.all(np.isfinite(y))
         assert np.all(np.abs(y[256:] - x[256:]) <= 3 * 2.0 ** -149)
+
+
+@pytest.mark.parametrize("bits", [1, 2, 4, 8])
+def test_threshold_ties_closed_form(orc, bits):
+    """T + u exactly on an integer N (q = N) and one fp32 step below / above it (q = N - 1 /
+    N): the closed form of q = floor(T + (2k+1) 2^-17) at its discontinuities (include/gact.h;
+    DESIGN.md R4, R5). Inputs from tests/tie_cases.py (mn = 0, inv = 1, so T = x exactly)."""
+    import tie_cases
+    seed = 0x7E5 + bits
+    x, want = tie_cases.tie_groups(6, 256, bits, seed, orc.lane16, np.random.default_rng(bits))
+    q, mn, sc = orc.quantize_codes(x, orc.F32, 256, bits, seed)
+    assert np.all(mn == 0.0) and np.all(sc == 1.0)
+    assert np.array_equal(q.astype(np.int64), want)
+    # the three cases all occur, for every b
+    ties = x[2:] != np.round(x[2:])
+    assert ties.sum() > 100
