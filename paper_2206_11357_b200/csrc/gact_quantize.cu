@@ -18,6 +18,7 @@
 //  * G in {32, 64, 128}: a tile holds 256/G groups of G/8 lanes; segmented shuffles.
 //  * G in {2048, 4096}: staged in shared memory (one HBM read).
 // A tensor's last tile may be partial (n % TE != 0): it takes the guarded generic path.
+#include <atomic>
 #include <cfloat>
 
 #include "gact_device.cuh"
@@ -28,6 +29,7 @@ namespace gact {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kMaxDevices = 64;
 
 template <int MAXB>
 __device__ __forceinline__ int advance_cursor(const QBatch<MAXB>& P, int cur, int64_t tile) {
@@ -522,10 +524,20 @@ cudaError_t launch_units(const PB& p, int64_t tiles_per_unit, cudaStream_t s, in
 template <int DT, int BITS, int MAXB, bool STATS, int NW>
 cudaError_t launch_staged_nw(const QBatch<MAXB>& p, int smem, cudaStream_t s) {
   constexpr auto kernel = quantize_staged_kernel<DT, BITS, MAXB, STATS, NW>;
-  static int configured = 0;  // largest dynamic smem size enabled so far
-  if (smem > configured) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    configured = smem;
+  // Largest dynamic shared-memory size enabled so far, per device (the attribute belongs to
+  // the device's context); atomic because the C ABI may be called from several host threads.
+  static std::atomic<int> configured[kMaxDevices];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<int>* done = dev >= 0 && dev < kMaxDevices ? &configured[dev] : nullptr;
+  if (!done || smem > done->load(std::memory_order_acquire)) {
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    if (done) {
+      int cur = done->load(std::memory_order_relaxed);
+      while (cur < smem && !done->compare_exchange_weak(cur, smem, std::memory_order_release)) {
+      }
+    }
   }
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, NW * 32, smem) != cudaSuccess || per_sm < 1)

@@ -307,3 +307,41 @@ def test_threshold_ties(gact, orc, bits, G):
     ct, ref = check_quantize(gact, orc, x, G, bits, seed)
     q = orc.unpack(host_bits(ct.packed), xh.size, bits).astype(np.int64)
     assert np.array_equal(q, want)
+
+
+def test_concurrent_host_threads(gact):
+    """The C ABI is stateless and thread-safe (include/gact.h): four host threads, each on its
+    own stream, compress and decompress their tensors repeatedly (G = 2048 bf16 exercises the
+    shared-memory kernel whose attribute is set once per device) and get exactly the results
+    of a single-threaded call."""
+    import threading
+    cases = [(make_input(200_000 + 4099 * i, (torch.bfloat16, torch.float32)[i % 2], seed=40 + i),
+              (1, 2, 4, 8)[i], 1000 + i, (2048, 256, 32, 4096)[i]) for i in range(4)]
+    ref = []
+    for x, b, s, G in cases:
+        ct = gact.quantize_pack(x, b, s, G)
+        ref.append((ct.packed.clone(), ct.group_min.clone(), ct.group_scale.clone(), ct.decompress().clone()))
+    torch.cuda.synchronize()
+    errors = []
+
+    def work(k):
+        try:
+            x, b, s, G = cases[k]
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                for _ in range(20):
+                    ct = gact.quantize_pack(x, b, s, G)
+                    y = ct.decompress()
+            st.synchronize()
+            p, mn, sc, yr = ref[k]
+            if not (torch.equal(ct.packed, p) and torch.equal(ct.group_min, mn)
+                    and torch.equal(ct.group_scale, sc) and torch.equal(y, yr)):
+                errors.append(f"thread {k}: results differ")
+        except Exception as e:  # surfaced below
+            errors.append(f"thread {k}: {e!r}")
+    th = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
