@@ -16,7 +16,7 @@ CSRC := $(PKG)/csrc
 OBJDIR := build/obj
 LIB_SRCS := $(wildcard $(CSRC)/*.cu)
 LIB_OBJS := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(LIB_SRCS))
-LIB_HDRS := include/gact.h $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h)
+LIB_HDRS := include/gact.h include/gact_testing.h $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h)
 
 all: lib oracle
 

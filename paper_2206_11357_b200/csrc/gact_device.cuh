@@ -109,6 +109,52 @@ __device__ __forceinline__ uint4 philox4x32_10(uint64_t block, uint32_t k0, uint
   return philox4x32_10_t<GACT_PHILOX_F64 != 0>(block, k0, k1);
 }
 
+// Philox4x32-10 of the four blocks blk + 32 m, m = 0..3 (a lane's blocks in one quantize
+// unit), bit-identical to four philox4x32_10 calls, with the work the four share done once.
+// When lo32(blk) + 96 does not wrap, all four counters are (c0 + 32 m, c1, 0, 0), so
+//   round 0: M0 (c0 + 32 m) = P_0 + m (32 M0) as 64-bit sums (one multiply, 3 adds); the
+//            outputs are (c1 ^ k0, 0, hi P_m ^ k1, lo P_m): word 0 is common to the four;
+//   round 1: M0 (c1 ^ k0) is common (one multiply instead of four);
+// rounds 2-9 run per block. A wrapping lo32 (tensors past 2^35 elements) takes four calls.
+__device__ __forceinline__ void philox4x32_10_x4(uint64_t blk, uint32_t k0, uint32_t k1, uint4 r[4]) {
+  const uint32_t c0 = (uint32_t)blk, c1 = (uint32_t)(blk >> 32);
+  if (c0 > 0xFFFFFFFFu - 96u) {
+#pragma unroll
+    for (int m = 0; m < 4; ++m) r[m] = philox4x32_10(blk + 32u * m, k0, k1);
+    return;
+  }
+  constexpr uint64_t kD = 32ull * 0xD2511F53ull;
+  const uint32_t x0 = c1 ^ k0;  // round-0 word 0, common
+  uint32_t L, H;                // round 1: M0 * x0, common
+  mul_wide(x0, 0xD2511F53u, L, H);
+  const uint32_t k0r1 = k0 + 0x9E3779B9u, k1r1 = k1 + 0xBB67AE85u;
+  uint64_t P = (uint64_t)c0 * 0xD2511F53u;
+#pragma unroll
+  for (int m = 0; m < 4; ++m, P += kD) {
+    const uint32_t p_lo = (uint32_t)P, p_hi = (uint32_t)(P >> 32);
+    // after round 0: (x0, 0, p_hi ^ k1, p_lo); round 1:
+    uint32_t lo1, hi1;
+    mul_wide(p_hi ^ k1, 0xCD9E8D57u, lo1, hi1);
+    uint32_t a0 = hi1 ^ k0r1, a1 = lo1, a2 = xor3(H, p_lo, k1r1), a3 = L;
+    uint32_t q0 = k0r1, q1 = k1r1;
+#pragma unroll
+    for (int rd = 2; rd < GACT_EXP_ROUNDS; ++rd) {
+      q0 += 0x9E3779B9u;
+      q1 += 0xBB67AE85u;
+      uint32_t l0, h0, l1, h1;
+      mul_wide(a0, 0xD2511F53u, l0, h0);
+      mul_wide(a2, 0xCD9E8D57u, l1, h1);
+      const uint32_t n0 = xor3(h1, a1, q0);
+      const uint32_t n2 = xor3(h0, a3, q1);
+      a1 = l1;
+      a3 = l0;
+      a0 = n0;
+      a2 = n2;
+    }
+    r[m] = make_uint4(a0, a1, a2, a3);
+  }
+}
+
 // ------------------------------------------------------------------- packed f32x2 math
 // sm_100a executes these as FADD2 / FMUL2 / FFMA2 (two lanes of fp32 per instruction),
 // each lane correctly rounded in the stated mode — identical to two scalar IEEE ops.

@@ -104,6 +104,9 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 #ifndef GACT_QS_MINB
 #define GACT_QS_MINB 3  // small-G kernel: minimum resident CTAs per SM (register cap)
 #endif
+#ifndef GACT_PHILOX_X4
+#define GACT_PHILOX_X4 1  // the 4 blocks of a lane by philox4x32_10_x4 (shared rounds 0-1)
+#endif
 #ifndef GACT_Q_RNG_EARLY
 #define GACT_Q_RNG_EARLY 64  // Philox blocks per lane computed while the unit's loads fly
 #endif
@@ -166,12 +169,24 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
     const uint32_t k0 = (uint32_t)T.seed, k1 = (uint32_t)(T.seed >> 32);
     const uint64_t blk = ((uint64_t)e_lane >> 3) + T.ctr0;
     if constexpr (!STATS) {
+      // Batched launches (MAXB > 1) only: measured +1.7% on the ResNet-50 context, but -5% on
+      // single-tensor launches, whose seed and key schedule are already uniform.
+      if constexpr (U * CPL == 4 && MAXB > 1 && GACT_Q_RNG_EARLY >= 4 && GACT_PHILOX_X4 && !GACT_PHILOX_F64) {
+        // block offsets (k TE + c 256) / 8 = 32 (k CPL + c): the shared-round form
+        uint4 r4[4];
+        philox4x32_10_x4(blk, k0, k1, r4);
 #pragma unroll
-      for (int k = 0; k < U; ++k)
+        for (int k = 0; k < U; ++k)
 #pragma unroll
-        for (int c = 0; c < CPL; ++c)
-          if (k * CPL + c < GACT_Q_RNG_EARLY)
-            rnd[k][c] = philox4x32_10(blk + (k * TE + c * kWarpTile) / kChunk, k0, k1);
+          for (int c = 0; c < CPL; ++c) rnd[k][c] = r4[k * CPL + c];
+      } else {
+#pragma unroll
+        for (int k = 0; k < U; ++k)
+#pragma unroll
+          for (int c = 0; c < CPL; ++c)
+            if (k * CPL + c < GACT_Q_RNG_EARLY)
+              rnd[k][c] = philox4x32_10(blk + (k * TE + c * kWarpTile) / kChunk, k0, k1);
+      }
     }
     float mnk[U], mxk[U];
 #pragma unroll

@@ -41,6 +41,18 @@ def test_exports_every_declared_symbol(L):
         assert getattr(L, n) is not None
 
 
+def test_exports_testing_entry_point(L):
+    """include/gact_testing.h (test-only generator access) is exported too."""
+    src = open(os.path.join(os.path.dirname(HEADER), "gact_testing.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = sorted(set(re.findall(r"\b(gact_[a-z_0-9]+)\s*\(", src)))
+    assert names == ["gact_test_philox_blocks"]
+    out = subprocess.run(["nm", "-D", "--defined-only", gact.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    assert "gact_test_philox_blocks" in set(re.findall(r"\bT (gact_\w+)", out))
+    assert L.gact_test_philox_blocks(0, 0, 1, None, None) == 1  # GACT_ERR_INVALID_ARG, no launch
+
+
 def test_no_oracle_linkage():
     """The product library neither links nor references the oracle."""
     out = subprocess.run(["nm", "-D", gact.LIB_PATH], capture_output=True, text=True, check=True).stdout
