@@ -109,18 +109,19 @@ __device__ __forceinline__ uint4 philox4x32_10(uint64_t block, uint32_t k0, uint
   return philox4x32_10_t<GACT_PHILOX_F64 != 0>(block, k0, k1);
 }
 
-// Philox4x32-10 of the four blocks blk + 32 m, m = 0..3 (a lane's blocks in one quantize
-// unit), bit-identical to four philox4x32_10 calls, with the work the four share done once.
-// When lo32(blk) + 96 does not wrap, all four counters are (c0 + 32 m, c1, 0, 0), so
-//   round 0: M0 (c0 + 32 m) = P_0 + m (32 M0) as 64-bit sums (one multiply, 3 adds); the
-//            outputs are (c1 ^ k0, 0, hi P_m ^ k1, lo P_m): word 0 is common to the four;
-//   round 1: M0 (c1 ^ k0) is common (one multiply instead of four);
-// rounds 2-9 run per block. A wrapping lo32 (tensors past 2^35 elements) takes four calls.
-__device__ __forceinline__ void philox4x32_10_x4(uint64_t blk, uint32_t k0, uint32_t k1, uint4 r[4]) {
+// Philox4x32-10 of the N blocks blk + 32 m, m = 0..N-1 (a lane's blocks in one quantize
+// unit), bit-identical to N philox4x32_10 calls, with the work they share done once. When
+// lo32(blk) + 32 (N - 1) does not wrap, every counter is (c0 + 32 m, c1, 0, 0), so
+//   round 0: M0 (c0 + 32 m) = P_0 + m (32 M0) as 64-bit sums (one multiply, N - 1 adds); the
+//            outputs are (c1 ^ k0, 0, hi P_m ^ k1, lo P_m): word 0 is common to all N;
+//   round 1: M0 (c1 ^ k0) is common (one multiply instead of N);
+// rounds 2-9 run per block. A wrapping lo32 (tensors past 2^35 elements) takes N calls.
+template <int N>
+__device__ __forceinline__ void philox4x32_10_xn(uint64_t blk, uint32_t k0, uint32_t k1, uint4 r[N]) {
   const uint32_t c0 = (uint32_t)blk, c1 = (uint32_t)(blk >> 32);
-  if (c0 > 0xFFFFFFFFu - 96u) {
+  if (c0 > 0xFFFFFFFFu - 32u * (N - 1)) {
 #pragma unroll
-    for (int m = 0; m < 4; ++m) r[m] = philox4x32_10(blk + 32u * m, k0, k1);
+    for (int m = 0; m < N; ++m) r[m] = philox4x32_10(blk + 32u * m, k0, k1);
     return;
   }
   constexpr uint64_t kD = 32ull * 0xD2511F53ull;
@@ -130,7 +131,7 @@ __device__ __forceinline__ void philox4x32_10_x4(uint64_t blk, uint32_t k0, uint
   const uint32_t k0r1 = k0 + 0x9E3779B9u, k1r1 = k1 + 0xBB67AE85u;
   uint64_t P = (uint64_t)c0 * 0xD2511F53u;
 #pragma unroll
-  for (int m = 0; m < 4; ++m, P += kD) {
+  for (int m = 0; m < N; ++m, P += kD) {
     const uint32_t p_lo = (uint32_t)P, p_hi = (uint32_t)(P >> 32);
     // after round 0: (x0, 0, p_hi ^ k1, p_lo); round 1:
     uint32_t lo1, hi1;
@@ -153,6 +154,9 @@ __device__ __forceinline__ void philox4x32_10_x4(uint64_t blk, uint32_t k0, uint
     }
     r[m] = make_uint4(a0, a1, a2, a3);
   }
+}
+__device__ __forceinline__ void philox4x32_10_x4(uint64_t blk, uint32_t k0, uint32_t k1, uint4 r[4]) {
+  philox4x32_10_xn<4>(blk, k0, k1, r);
 }
 
 // ------------------------------------------------------------------- packed f32x2 math

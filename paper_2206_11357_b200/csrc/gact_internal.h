@@ -76,8 +76,8 @@ cudaError_t launch_dequantize(const DBatch<MAXB>& p, int dtype, int bits, cudaSt
 
 inline int64_t quantize_tile_elems(int log2g) { return log2g >= 8 ? (int64_t(1) << log2g) : 256; }
 // Each tensor's quantize tile count is rounded up to this, so that a CTA unit (8 warps x up
-// to 4 consecutive tiles) never straddles two tensors of a batch.
-constexpr int64_t kTileAlign = 32;
+// to 8 consecutive tiles) never straddles two tensors of a batch.
+constexpr int64_t kTileAlign = 64;
 inline int64_t quantize_tiles(int64_t n, int log2g) {
   const int64_t te = quantize_tile_elems(log2g);
   const int64_t t = (n + te - 1) / te;

@@ -90,7 +90,7 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 }
 
 // ---------------------------------------------------------------------------------------
-// G in {256, 512, 1024}: CPL = G/256 chunks per lane, U = kQuantUnit/CPL tiles per unit,
+// G in {256, 512, 1024}: CPL = G/256 chunks per lane, U = quant_unit<DT>()/CPL tiles per unit,
 // all in registers.
 // Grid = waves x resident CTAs. Several waves (CTAs pick up units dynamically as others
 // retire) beat a persistent grid for the FMA-bound 2-byte inputs (+6% at bf16); fp32 inputs
@@ -113,19 +113,31 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 #ifndef GACT_Q_PREFETCH
 #define GACT_Q_PREFETCH 0
 #endif
+// Chunks (Philox blocks) per lane per CTA unit: 8 for 2-byte inputs (FMA-bound: the unit's
+// 8 blocks share Philox rounds 0-1 and the key schedule / bookkeeping is amortised over 8
+// tiles; ~124 registers, 2 CTAs per SM), 4 for fp32 (HBM-bound; 8 would spill).
 #ifndef GACT_Q_UNIT
-#define GACT_Q_UNIT 4
+#define GACT_Q_UNIT 8
+#endif
+#ifndef GACT_Q_UNIT_F32
+#define GACT_Q_UNIT_F32 4
 #endif
 #ifndef GACT_Q_MINB
 #define GACT_Q_MINB 2
 #endif
-constexpr int kQuantUnit = GACT_Q_UNIT;
-static_assert(kQuantUnit <= kTileAlign && kTileAlign % kQuantUnit == 0, "unit must divide the tile alignment");
+template <int DT>
+__host__ __device__ constexpr int quant_unit() { return DT == DT_F32 ? GACT_Q_UNIT_F32 : GACT_Q_UNIT; }
+// tiles per warp per unit for G = 256 CPL
+template <int DT, int CPL>
+__host__ __device__ constexpr int unit_tiles() { return quant_unit<DT>() / CPL > 0 ? quant_unit<DT>() / CPL : 1; }
+static_assert(kWarps * GACT_Q_UNIT <= kTileAlign && kTileAlign % (kWarps * GACT_Q_UNIT) == 0 &&
+              kWarps * GACT_Q_UNIT_F32 <= kTileAlign && kTileAlign % (kWarps * GACT_Q_UNIT_F32) == 0,
+              "a CTA unit must divide the tile alignment");
 
 template <int DT, int BITS, int CPL, int MAXB, bool STATS>
 __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
     quantize_big_kernel(const __grid_constant__ QBatch<MAXB> P) {
-  constexpr int U = kQuantUnit / CPL > 0 ? kQuantUnit / CPL : 1;
+  constexpr int U = unit_tiles<DT, CPL>();
   constexpr int TE = CPL * kWarpTile;  // == G
   constexpr int CU = kWarps * U;       // tiles per CTA unit (divides kTileAlign)
   const int lane = threadIdx.x & 31;
@@ -171,10 +183,10 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
     if constexpr (!STATS) {
       // Batched launches (MAXB > 1) only: measured +1.7% on the ResNet-50 context, but -5% on
       // single-tensor launches, whose seed and key schedule are already uniform.
-      if constexpr (U * CPL == 4 && MAXB > 1 && GACT_Q_RNG_EARLY >= 4 && GACT_PHILOX_X4 && !GACT_PHILOX_F64) {
+      if constexpr (MAXB > 1 && GACT_Q_RNG_EARLY >= U * CPL && GACT_PHILOX_X4 && !GACT_PHILOX_F64) {
         // block offsets (k TE + c 256) / 8 = 32 (k CPL + c): the shared-round form
-        uint4 r4[4];
-        philox4x32_10_x4(blk, k0, k1, r4);
+        uint4 r4[U * CPL];
+        philox4x32_10_xn<U * CPL>(blk, k0, k1, r4);
 #pragma unroll
         for (int k = 0; k < U; ++k)
 #pragma unroll
@@ -584,11 +596,11 @@ cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
     case 7:
       return launch_persistent<quantize_small_kernel<DT, BITS, MAXB, STATS, 7>>(p, 4, s, waves);
     case 8:
-      return launch_persistent<quantize_big_kernel<DT, BITS, 1, MAXB, STATS>>(p, kQuantUnit, s, waves);
+      return launch_persistent<quantize_big_kernel<DT, BITS, 1, MAXB, STATS>>(p, unit_tiles<DT, 1>(), s, waves);
     case 9:
-      return launch_persistent<quantize_big_kernel<DT, BITS, 2, MAXB, STATS>>(p, kQuantUnit / 2, s, waves);
+      return launch_persistent<quantize_big_kernel<DT, BITS, 2, MAXB, STATS>>(p, unit_tiles<DT, 2>(), s, waves);
     case 10:
-      return launch_persistent<quantize_big_kernel<DT, BITS, 4, MAXB, STATS>>(p, kQuantUnit > 4 ? kQuantUnit / 4 : 1, s, waves);
+      return launch_persistent<quantize_big_kernel<DT, BITS, 4, MAXB, STATS>>(p, unit_tiles<DT, 4>(), s, waves);
     default:
       // fp32 (HBM-bound): the group spread over the CTA in registers (+10-24%); 2-byte inputs
       // (FMA-bound): the per-warp shared-memory stage, which needs no CTA barrier.
