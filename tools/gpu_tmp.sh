@@ -1,16 +1,4 @@
 #!/bin/bash
 cd "$(dirname "$0")/.."
-make oracle >/dev/null
-echo "default tests: $(timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider 2>&1 | tail -1)"
-for pass in 1 2; do
-for d in default build/var_u4; do
-  lib=paper_2206_11357_b200/libgact.so; [ "$d" != default ] && lib=$d/libgact.so
-  for spec in "268435456 bf16 1" "268435456 bf16 4" "268435456 bf16 8" "268435456 f16 2" "268435456 f32 4"; do set -- $spec
-    echo "$pass $d $(GACT_LIB_PATH=$lib python tools/prof_kernels.py --n $1 --dtype $2 --bits $3 --reps 1 2>&1 | tail -1)"
-  done
-  for w in "resnet50 bf16" "resnet50 f32" "bert_layer bf16" "gcn_swin bf16"; do set -- $w
-  echo "$pass $d $1 $2 $(GACT_LIB_PATH=$lib python bench.py --workload $1 --dtype $2 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['phases']['quantize_ms'])")"
-  done
-done
-done
-exit 0
+bash tools/gpu_check.sh r01d
+bash tools/gpu_bench_all.sh r01d
