@@ -107,6 +107,9 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 #ifndef GACT_PHILOX_X4
 #define GACT_PHILOX_X4 1  // the 4 blocks of a lane by philox4x32_10_x4 (shared rounds 0-1)
 #endif
+#ifndef GACT_PHILOX_X4_F32
+#define GACT_PHILOX_X4_F32 1
+#endif
 #ifndef GACT_Q_RNG_EARLY
 #define GACT_Q_RNG_EARLY 64  // Philox blocks per lane computed while the unit's loads fly
 #endif
@@ -125,6 +128,9 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 #ifndef GACT_Q_MINB
 #define GACT_Q_MINB 2
 #endif
+#ifndef GACT_Q_MINB_F32
+#define GACT_Q_MINB_F32 2
+#endif
 template <int DT>
 __host__ __device__ constexpr int quant_unit() { return DT == DT_F32 ? GACT_Q_UNIT_F32 : GACT_Q_UNIT; }
 // tiles per warp per unit for G = 256 CPL
@@ -135,7 +141,7 @@ static_assert(kWarps * GACT_Q_UNIT <= kTileAlign && kTileAlign % (kWarps * GACT_
               "a CTA unit must divide the tile alignment");
 
 template <int DT, int BITS, int CPL, int MAXB, bool STATS>
-__global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
+__global__ void __launch_bounds__(kThreads, DT == DT_F32 ? GACT_Q_MINB_F32 : GACT_Q_MINB)
     quantize_big_kernel(const __grid_constant__ QBatch<MAXB> P) {
   constexpr int U = unit_tiles<DT, CPL>();
   constexpr int TE = CPL * kWarpTile;  // == G
@@ -183,7 +189,8 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
     if constexpr (!STATS) {
       // Batched launches (MAXB > 1) only: measured +1.7% on the ResNet-50 context, but -5% on
       // single-tensor launches, whose seed and key schedule are already uniform.
-      if constexpr (MAXB > 1 && GACT_Q_RNG_EARLY >= U * CPL && GACT_PHILOX_X4 && !GACT_PHILOX_F64) {
+      if constexpr (MAXB > 1 && (DT != DT_F32 || GACT_PHILOX_X4_F32) && GACT_Q_RNG_EARLY >= U * CPL &&
+                    GACT_PHILOX_X4 && !GACT_PHILOX_F64) {
         // block offsets (k TE + c 256) / 8 = 32 (k CPL + c): the shared-round form
         uint4 r4[U * CPL];
         philox4x32_10_xn<U * CPL>(blk, k0, k1, r4);
