@@ -5,16 +5,18 @@
 // elements; a warp owns a tile at a time and each lane a chunk of 8 consecutive elements
 // (one Philox4x32-10 call = 8 x 16-bit lanes; one 16- or 32-byte coalesced load).
 // Tensors of a batch are concatenated in tile space (QBatch::tile_start), each tensor's
-// tile count rounded up to kTileAlign = 32, so that a CTA UNIT (8 warps x U consecutive
+// tile count rounded up to kTileAlign = 64, so that a CTA UNIT (8 warps x U consecutive
 // tiles) never straddles two tensors. CTAs walk units grid-stride: the active window of a
 // launch is compact in memory, each warp streams U * TE contiguous elements per step, and
-// the unit's bookkeeping (tensor, seed, pointers) is warp-uniform AND CTA-uniform, so it
-// lives in the uniform datapath (UIADD3 key schedule for Philox).
+// the unit's bookkeeping (tensor, seed, pointers) is CTA-uniform (single-tensor launches
+// keep it in the uniform datapath; batched launches index the descriptor table per unit).
 //  * G in {256, 512, 1024}: one tile == one group, reduced in registers (FMNMX3 in-thread,
 //    one CREDUX per warp for min and max), coded from the same registers, written once:
-//    x is read exactly once. The U x CPL Philox blocks of a unit are computed while its
-//    loads are in flight (they depend only on (seed, element index)); the U groups'
-//    divisions run on U lanes and are broadcast with one shuffle.
+//    x is read exactly once. The U x CPL (8 for 2-byte inputs, 4 for fp32) Philox blocks
+//    of a lane are computed while the unit's loads are in flight (they depend only on
+//    (seed, element index)); batched launches share their rounds 0-1
+//    (philox4x32_10_xn). The U groups' divisions run on U lanes and are broadcast with
+//    one shuffle each.
 //  * G in {32, 64, 128}: a tile holds 256/G groups of G/8 lanes; segmented shuffles.
 //  * G in {2048, 4096}: staged in shared memory (one HBM read).
 // A tensor's last tile may be partial (n % TE != 0): it takes the guarded generic path.
