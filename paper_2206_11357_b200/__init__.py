@@ -90,7 +90,7 @@ def lib() -> ctypes.CDLL:
             "gact_sq_diff_sum": (i32, [P, P, i32, i64, P, P, P]),
             "gact_quantize_pack_staged": (i32, [ctypes.POINTER(_Desc), i32, i32, P, u64, P]),
             "gact_unpack_dequantize_staged": (i32, [ctypes.POINTER(_Desc), i32, i32, P, u64, P]),
-            "gact_test_philox_blocks": (i32, [u64, u64, i32, P, P]),  # include/gact_testing.h
+            "gact_test_philox_blocks": (i32, [u64, u64, i32, i32, P, P]),  # include/gact_testing.h
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)

@@ -5,16 +5,17 @@
 
 namespace {
 
+template <int N>
 __global__ void philox_blocks_kernel(uint64_t blk, uint64_t seed, int shared_form, uint32_t* out) {
   const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
-  uint4 r[4];
+  uint4 r[N];
   if (shared_form) {
-    gact::philox4x32_10_x4(blk, k0, k1, r);
+    gact::philox4x32_10_xn<N>(blk, k0, k1, r);
   } else {
 #pragma unroll
-    for (int m = 0; m < 4; ++m) r[m] = gact::philox4x32_10(blk + 32u * m, k0, k1);
+    for (int m = 0; m < N; ++m) r[m] = gact::philox4x32_10(blk + 32u * m, k0, k1);
   }
-  for (int m = 0; m < 4; ++m) {
+  for (int m = 0; m < N; ++m) {
     out[4 * m + 0] = r[m].x;
     out[4 * m + 1] = r[m].y;
     out[4 * m + 2] = r[m].z;
@@ -25,8 +26,10 @@ __global__ void philox_blocks_kernel(uint64_t blk, uint64_t seed, int shared_for
 }  // namespace
 
 extern "C" gact_status gact_test_philox_blocks(uint64_t blk, uint64_t seed, int32_t shared_form,
-                                               uint32_t* out, void* stream) {
-  if (!out) return GACT_ERR_INVALID_ARG;
-  philox_blocks_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(blk, seed, shared_form, out);
+                                               int32_t n_blocks, uint32_t* out, void* stream) {
+  if (!out || (n_blocks != 4 && n_blocks != 8)) return GACT_ERR_INVALID_ARG;
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (n_blocks == 4) philox_blocks_kernel<4><<<1, 1, 0, s>>>(blk, seed, shared_form, out);
+  else philox_blocks_kernel<8><<<1, 1, 0, s>>>(blk, seed, shared_form, out);
   return cudaPeekAtLastError() == cudaSuccess ? GACT_OK : GACT_ERR_CUDA;
 }

@@ -50,7 +50,9 @@ def test_exports_testing_entry_point(L):
     out = subprocess.run(["nm", "-D", "--defined-only", gact.LIB_PATH], capture_output=True,
                          text=True, check=True).stdout
     assert "gact_test_philox_blocks" in set(re.findall(r"\bT (gact_\w+)", out))
-    assert L.gact_test_philox_blocks(0, 0, 1, None, None) == 1  # GACT_ERR_INVALID_ARG, no launch
+    assert L.gact_test_philox_blocks(0, 0, 1, 4, None, None) == 1  # GACT_ERR_INVALID_ARG, no launch
+    out = ctypes.c_void_p(16)  # never dereferenced: rejected before any launch
+    assert L.gact_test_philox_blocks(0, 0, 1, 5, out, None) == 1
 
 
 def test_no_oracle_linkage():

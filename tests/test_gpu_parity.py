@@ -347,25 +347,28 @@ def test_concurrent_host_threads(gact):
     assert not errors, errors
 
 
+@pytest.mark.parametrize("nblk", [4, 8])
 @pytest.mark.parametrize("shared", [1, 0], ids=["shared_rounds", "plain"])
-def test_philox_blocks_at_counter_boundaries(gact, orc, shared):
+def test_philox_blocks_at_counter_boundaries(gact, orc, shared, nblk):
     """The device generator (include/gact_testing.h) at the counters where the batched
-    kernels' shared-round Philox form switches to its fallback (lo32(blk) + 96 wrapping) and
-    across the 2^32 carry into the counter's high word, against the oracle's Philox4x32-10."""
+    kernels' shared-round Philox form (N = 4 fp32, N = 8 bf16/fp16 blocks per lane) switches
+    to its fallback (lo32(blk) + 32 (N - 1) wrapping) and across the 2^32 carry into the
+    counter's high word, against the oracle's Philox4x32-10."""
     L = gact.lib()
-    out = torch.zeros(16, dtype=torch.int32, device="cuda")
+    out = torch.zeros(4 * nblk, dtype=torch.int32, device="cuda")
     rng = np.random.default_rng(7)
     seeds = [0, 0x5EED, 0xFFFFFFFFFFFFFFFF, int(rng.integers(0, 2**63))]
     top = 2**32
-    blks = [0, 1, 31, 32, 96, top - 200, top - 97, top - 96, top - 95, top - 64, top - 33, top - 32,
-            top - 1, top, top + 5, 5 * top - 96, 2**40 - 97, 2**63 + 12345] + \
-           [int(v) for v in rng.integers(0, 2**62, 8)]
+    edge = 32 * (nblk - 1)
+    blks = [0, 1, 31, 32, 96, 224, top - 300, top - edge - 2, top - edge - 1, top - edge, top - edge + 1,
+            top - 97, top - 96, top - 95, top - 33, top - 32, top - 1, top, top + 5, 5 * top - edge,
+            2**40 - edge - 1, 2**63 + 12345] + [int(v) for v in rng.integers(0, 2**62, 8)]
     for seed in seeds:
         for blk in blks:
-            assert L.gact_test_philox_blocks(blk, seed, shared, out.data_ptr(), None) == 0
+            assert L.gact_test_philox_blocks(blk, seed, shared, nblk, out.data_ptr(), None) == 0
             torch.cuda.synchronize()
             got = out.cpu().numpy().view(np.uint32)
-            for m in range(4):
+            for m in range(nblk):
                 b = (blk + 32 * m) % 2**64
                 ref = orc.philox4x32_10([b & 0xFFFFFFFF, b >> 32, 0, 0], [seed & 0xFFFFFFFF, seed >> 32])
                 assert np.array_equal(got[4 * m: 4 * m + 4], ref), (hex(blk), m, hex(seed))
