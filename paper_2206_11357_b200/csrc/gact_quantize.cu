@@ -456,10 +456,8 @@ __global__ void __launch_bounds__(kThreads, GACT_QS_MINB)
     for (int k = 0; k < U; ++k)
       if (e_warp + (k + 1) * kWarpTile <= T.n) load8<DT>(raw[k], T.x, e_lane + k * kWarpTile);
     if constexpr (!STATS) {
-#pragma unroll
-      for (int k = 0; k < U; ++k)
-        rnd[k] = philox4x32_10(((uint64_t)e_lane >> 3) + T.ctr0 + k * (kWarpTile / kChunk), (uint32_t)T.seed,
-                               (uint32_t)(T.seed >> 32));
+      // blocks blk + 32 k: the shared-round form (philox4x32_10_xn)
+      philox4x32_10_xn<U>(((uint64_t)e_lane >> 3) + T.ctr0, (uint32_t)T.seed, (uint32_t)(T.seed >> 32), rnd);
     }
     if (e_warp + U * kWarpTile > T.n) {  // the tensor's last unit: tile by tile, guarded
 #pragma unroll
