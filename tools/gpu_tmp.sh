@@ -1,21 +1,5 @@
 #!/bin/bash
 cd "$(dirname "$0")/.."
-python - <<'PY'
-import torch, time
-n = 2 << 30
-h = torch.empty(n, dtype=torch.uint8, pin_memory=True); d = torch.empty(n, dtype=torch.uint8, device='cuda')
-h2 = torch.empty(n, dtype=torch.uint8, pin_memory=True); d2 = torch.empty(n, dtype=torch.uint8, device='cuda')
-for name, fn in [("H2D", lambda: d.copy_(h, non_blocking=True)), ("D2H", lambda: h.copy_(d, non_blocking=True))]:
-    fn(); torch.cuda.synchronize()
-    t = time.perf_counter()
-    for _ in range(5): fn()
-    torch.cuda.synchronize()
-    print(name, round(5 * n / (time.perf_counter() - t) / 1e9, 1), "GB/s")
-s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
-torch.cuda.synchronize(); t = time.perf_counter()
-for _ in range(5):
-    with torch.cuda.stream(s1): d.copy_(h, non_blocking=True)
-    with torch.cuda.stream(s2): h2.copy_(d2, non_blocking=True)
-torch.cuda.synchronize()
-print("bidirectional H2D+D2H each", round(5 * n / (time.perf_counter() - t) / 1e9, 1), "GB/s")
-PY
+for dt in bf16 f32; do for G in 32 64 128 256 512 1024 2048 4096; do
+  python tools/prof_kernels.py --G $G --dtype $dt --bits 4 --reps 1 2>&1 | tail -1
+done; done
