@@ -10,7 +10,7 @@
 // launch is compact in memory, each warp streams U * TE contiguous elements per step, and
 // the unit's bookkeeping (tensor, seed, pointers) is CTA-uniform (single-tensor launches
 // keep it in the uniform datapath; batched launches index the descriptor table per unit).
-//  * G in {256, 512, 1024}: one tile == one group, reduced in registers (FMNMX3 in-thread,
+//  * G in {256, 512, 1024} (and 2048 for 2-byte inputs): one tile == one group, reduced in registers (FMNMX3 in-thread,
 //    one CREDUX per warp for min and max), coded from the same registers, written once:
 //    x is read exactly once. The U x CPL (8 for 2-byte inputs, 4 for fp32) Philox blocks
 //    of a lane are computed while the unit's loads are in flight (they depend only on
@@ -92,7 +92,7 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 }
 
 // ---------------------------------------------------------------------------------------
-// G in {256, 512, 1024}: CPL = G/256 chunks per lane, U = quant_unit<DT>()/CPL tiles per unit,
+// G in {256, 512, 1024} (2048 for 2-byte inputs): CPL = G/256 chunks per lane, U = quant_unit<DT>()/CPL tiles per unit,
 // all in registers.
 // Grid = waves x resident CTAs. Several waves (CTAs pick up units dynamically as others
 // retire) beat a persistent grid for the FMA-bound 2-byte inputs (+6% at bf16); fp32 inputs
@@ -126,6 +126,9 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 #endif
 #ifndef GACT_Q_UNIT_F32
 #define GACT_Q_UNIT_F32 4
+#endif
+#ifndef GACT_Q_G2048_REGS
+#define GACT_Q_G2048_REGS 1
 #endif
 #ifndef GACT_Q_MINB
 #define GACT_Q_MINB 2
@@ -608,6 +611,12 @@ cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
       return launch_persistent<quantize_big_kernel<DT, BITS, 2, MAXB, STATS>>(p, unit_tiles<DT, 2>(), s, waves);
     case 10:
       return launch_persistent<quantize_big_kernel<DT, BITS, 4, MAXB, STATS>>(p, unit_tiles<DT, 4>(), s, waves);
+    case 11:
+      // 2-byte inputs, G = 2048: one group per warp, 8 chunks per lane, all in registers
+      // (the 8-chunk unit of G = 256 with U = 1 tile), read once.
+      if constexpr (DT != DT_F32 && GACT_Q_G2048_REGS)
+        return launch_persistent<quantize_big_kernel<DT, BITS, 8, MAXB, STATS>>(p, unit_tiles<DT, 8>(), s, waves);
+      [[fallthrough]];
     default:
       // fp32 (HBM-bound): the group spread over the CTA in registers (+10-24%); 2-byte inputs
       // (FMA-bound): the per-warp shared-memory stage, which needs no CTA barrier.
