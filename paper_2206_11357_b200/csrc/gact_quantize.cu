@@ -18,7 +18,8 @@
 //    (philox4x32_10_xn). The U groups' divisions run on U lanes and are broadcast with
 //    one shuffle each.
 //  * G in {32, 64, 128}: a tile holds 256/G groups of G/8 lanes; segmented shuffles.
-//  * G in {2048, 4096}: staged in shared memory (one HBM read).
+//  * G = 4096 (2-byte inputs): staged in shared memory; G in {2048, 4096} fp32: the group
+//    spans the CTA's registers (one HBM read either way).
 // A tensor's last tile may be partial (n % TE != 0): it takes the guarded generic path.
 #include <atomic>
 #include <cfloat>
@@ -254,7 +255,8 @@ __global__ void __launch_bounds__(kThreads, DT == DT_F32 ? GACT_Q_MINB_F32 : GAC
 }
 
 // ---------------------------------------------------------------------------------------
-// G in {2048, 4096}, 2-byte inputs: the group does not fit in one warp's registers. Pass 1
+// G = 4096 (and G = 2048 with GACT_Q_G2048_REGS=0), 2-byte inputs: the group does not fit in
+// one warp's registers. Pass 1
 // streams it from HBM once,
 // folding min/max and parking each lane's chunks in shared memory (G * s_in bytes per warp,
 // each lane re-reads only what it wrote: no synchronisation); pass 2 codes from shared memory.
