@@ -256,9 +256,7 @@ __global__ void __launch_bounds__(kThreads, DT == DT_F32 ? GACT_Q_MINB_F32 : GAC
 
 // ---------------------------------------------------------------------------------------
 // G = 4096 (and G = 2048 with GACT_Q_G2048_REGS=0), 2-byte inputs: the group does not fit in
-// one warp's registers. Pass 1
-// streams it from HBM once,
-// folding min/max and parking each lane's chunks in shared memory (G * s_in bytes per warp,
+// one warp's registers. Pass 1 streams it from HBM once, folding min/max and parking each lane's chunks in shared memory (G * s_in bytes per warp,
 // each lane re-reads only what it wrote: no synchronisation); pass 2 codes from shared memory.
 template <int DT, int BITS, int MAXB, bool STATS, int NW>
 __global__ void __launch_bounds__(NW * 32)
