@@ -55,7 +55,24 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--dry-run", action="store_true",
+                   help="host path only (launch, process group, a7 merge, a6 allocation); no kernels, no value")
     return p.parse_args()
+
+
+def self_launch(args) -> int:
+    """`python bench.py --gpus N` (N > 1) outside torchrun: start N ranks on this node the way
+    the driver does (torch.distributed.run, 127.0.0.1) and return their exit status. Rank 0's
+    JSON line passes through on stdout."""
+    import socket
+    import subprocess
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=dict(os.environ, MASTER_ADDR="127.0.0.1"))
 
 
 def dist_env():
@@ -141,10 +158,15 @@ def run_ours(args):
     from paper_2206_11357_b200 import dist as gdist
 
     rank, world, local = dist_env()
+    backend = os.environ.get("GACT_DIST_BACKEND", "nccl")  # gloo: functional test of the N > 1
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product path has no CPU fallback)")
+    if backend == "nccl" and world > torch.cuda.device_count():
+        raise SystemExit(f"bench.py: {world} ranks over NCCL need {world} GPUs, "
+                         f"this node has {torch.cuda.device_count()}")
     local = local % max(1, torch.cuda.device_count())  # several ranks per GPU only in gloo tests
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    backend = os.environ.get("GACT_DIST_BACKEND", "nccl")  # gloo: functional test of the N > 1
     if world > 1:                                           # path with several ranks on one GPU
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
@@ -475,7 +497,7 @@ def run_reference(args):
     sample = f"first {32 * G} elements of each of the {len(specs)} tensors, b={bits}, per step"
     print(json.dumps({
         "impl": "reference", "metric": "quantize+pack / dequant GB/s per B200 (% of HBM peak); activation compression",
-        "value": round(val, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "value": round(val, 4), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(secs / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded)",
         "config": {"workload": WORKLOAD_CONFIG.get(args.workload, args.workload), "group_size": G,
@@ -486,10 +508,47 @@ def run_reference(args):
     }), flush=True)
 
 
+def run_dry(args):
+    """--dry-run: the launch and host side of a step at N ranks (gloo process group, the a7
+    all-reduce of c, the a6 greedy in libgact, the cross-rank agreement check) without kernels.
+    Prints a JSON line with "value": null; used by the CPU tests of the N > 1 launch path."""
+    import torch.distributed as dist
+
+    import paper_2206_11357_b200 as gact
+    from paper_2206_11357_b200 import dist as gdist
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    avg_bits = args.avg_bits if args.avg_bits is not None else WORKLOAD_BITS[args.workload]
+    specs = synth.workload_specs(args.workload)
+    D = np.array([s.numel for s in specs], dtype=np.int64)
+    c = gdist.merge_sensitivities(synth.sensitivities(specs, seed=7, rank=rank))
+    bits = gact.allocate_bits(c, D, int(avg_bits * D.sum()))
+    gdist.assert_same_allocation(bits)
+    if rank == 0:
+        hist = {}
+        for b in bits:
+            hist[str(int(b))] = hist.get(str(int(b)), 0) + 1
+        print(json.dumps({"dry_run": True, "value": None, "n_gpus": world, "steps": 0,
+                          "config": {"workload": WORKLOAD_CONFIG.get(args.workload, args.workload),
+                                     "bits_histogram": hist}}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
+    launched = "WORLD_SIZE" in os.environ
+    if not launched and args.gpus > 1:
+        sys.exit(self_launch(args))
+    rank, world, _ = dist_env()
+    if launched and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args)
+    elif args.dry_run:
+        run_dry(args)
     else:
         run_ours(args)
 

@@ -208,6 +208,13 @@ gact_status gact_allocate_bits(const double* sensitivity, const int64_t* numel, 
                                const int32_t* ladder, int32_t n_ladder, uint64_t budget_bits,
                                int32_t* bits_out);
 
+/* S(b) = (2^b - 1)^-2, the per-tensor variance factor of P:479-480 (Var of the b-bit
+ * quantizer <= 1/4 range^2 S(b)), with S(32) = 0 (32 bits = uncompressed): the S the
+ * allocator above uses, exposed so that callers of Alg. 1 (c_l = 1/2 ||g0 - g1||^2 / S(b_l),
+ * P:524) and of the variance prediction sum_l c_l S(b_l) use the same
+ * definition. Host function. bits in [1, 16] or 32; any other value returns -1.0. */
+double gact_variance_factor(int32_t bits);
+
 /* NEXT-3 — the reduction of Alg. 1: sum_i (a_i - b_i)^2 of two gradient
  * vectors g0, g1 (one fwd+bwd each, seeds differing only for tensor l), from which
  * c_l = 1/2 ||g0 - g1||^2 / S(b_l). Deterministic: a fixed grid of GACT_REDUCE_BLOCKS

@@ -26,7 +26,7 @@ __all__ = [
     "lib", "GactError", "F32", "BF16", "F16", "DEFAULT_GROUP", "LADDER",
     "num_groups", "packed_words", "group_stats", "quantize_pack", "unpack_dequantize",
     "quantize_pack_batch", "unpack_dequantize_batch", "allocate_bits", "CompressedTensor",
-    "sq_diff_sum", "S", "BatchPlan", "quantize_pack_staged", "unpack_dequantize_staged",
+    "sq_diff_sum", "variance_factor", "BatchPlan", "quantize_pack_staged", "unpack_dequantize_staged",
     "staged_workspace",
 ]
 
@@ -87,6 +87,7 @@ def lib() -> ctypes.CDLL:
             "gact_quantize_pack_batch": (i32, [ctypes.POINTER(_Desc), i32, i32, P]),
             "gact_unpack_dequantize_batch": (i32, [ctypes.POINTER(_Desc), i32, i32, P]),
             "gact_allocate_bits": (i32, [P, P, i32, P, i32, u64, P]),
+            "gact_variance_factor": (ctypes.c_double, [i32]),
             "gact_sq_diff_sum": (i32, [P, P, i32, i64, P, P, P]),
             "gact_quantize_pack_staged": (i32, [ctypes.POINTER(_Desc), i32, i32, P, u64, P]),
             "gact_unpack_dequantize_staged": (i32, [ctypes.POINTER(_Desc), i32, i32, P, u64, P]),
@@ -113,6 +114,36 @@ def _require_cuda(*ts: torch.Tensor) -> None:
     for t in ts:
         if not t.is_cuda:
             raise ValueError("libgact runs on CUDA tensors only (no CPU fallback)")
+
+
+def _need(t: torch.Tensor, numel: int, dtype, device, what: str) -> None:
+    """A caller-supplied buffer the kernels will read or write: it must be a contiguous CUDA
+    tensor of `dtype` on `device` with at least `numel` elements (checked before any call,
+    so a short or strided buffer raises instead of being written out of bounds)."""
+    if not t.is_cuda or t.device != device:
+        raise ValueError(f"{what}: must be on {device}, got {t.device}")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{what}: dtype {t.dtype}, expected {dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what}: must be contiguous")
+    if t.numel() < numel:
+        raise ValueError(f"{what}: {t.numel()} elements, needs >= {numel}")
+
+
+def _aligned(x: torch.Tensor) -> torch.Tensor:
+    """x contiguous and 16-byte aligned (the C ABI's requirement): a view whose storage offset
+    breaks the alignment (x[1:], an odd split) is copied once."""
+    x = x.contiguous()
+    if x.data_ptr() % 16:
+        x = x.clone()
+    return x
+
+
+def _codes_need(packed, group_min, group_scale, n, bits, group_size, device, what):
+    _need(packed, max(packed_words(n, bits), 0), torch.int32, device, f"{what}: packed")
+    ng = max(num_groups(n, group_size), 0)
+    _need(group_min, ng, torch.float32, device, f"{what}: group_min")
+    _need(group_scale, ng, torch.float32, device, f"{what}: group_scale")
 
 
 def num_groups(n: int, group_size: int = DEFAULT_GROUP) -> int:
@@ -150,7 +181,7 @@ class CompressedTensor:
 def group_stats(x: torch.Tensor, bits: int, group_size: int = DEFAULT_GROUP):
     """Per-group (min, scale) of a CUDA tensor (flattened row-major)."""
     _require_cuda(x)
-    x = x.contiguous()
+    x = _aligned(x)
     n = x.numel()
     ng = max(num_groups(n, group_size), 0)
     mn = torch.empty(ng, dtype=torch.float32, device=x.device)
@@ -164,7 +195,7 @@ def quantize_pack(x: torch.Tensor, bits: int, seed: int, group_size: int = DEFAU
                   out: tuple | None = None) -> CompressedTensor:
     """Compress one context tensor: fused group min/max + stochastic rounding + packing."""
     _require_cuda(x)
-    xc = x.contiguous()
+    xc = _aligned(x)
     n = xc.numel()
     if out is None:
         packed = torch.empty(max(packed_words(n, bits), 0), dtype=torch.int32, device=x.device)
@@ -172,6 +203,7 @@ def quantize_pack(x: torch.Tensor, bits: int, seed: int, group_size: int = DEFAU
         sc = torch.empty_like(mn)
     else:
         packed, mn, sc = out
+        _codes_need(packed, mn, sc, n, bits, group_size, x.device, "quantize_pack out")
     _check("gact_quantize_pack", lib().gact_quantize_pack(
         xc.data_ptr(), _TORCH_TAG[x.dtype], n, group_size, bits, seed & (2**64 - 1),
         packed.data_ptr(), mn.data_ptr(), sc.data_ptr(), _stream(xc)))
@@ -183,7 +215,14 @@ def unpack_dequantize(packed: torch.Tensor, group_min: torch.Tensor, group_scale
                       dtype: torch.dtype = torch.float32, out: torch.Tensor | None = None) -> torch.Tensor:
     """Decompress: y = RNE_dtype(fma(q, scale, mn)) for n elements."""
     _require_cuda(packed, group_min, group_scale)
-    y = torch.empty(n, dtype=dtype, device=packed.device) if out is None else out
+    _codes_need(packed, group_min, group_scale, n, bits, group_size, packed.device, "unpack_dequantize")
+    if out is None:
+        y = torch.empty(n, dtype=dtype, device=packed.device)
+    else:
+        y = out
+        _need(y, n, None, packed.device, "unpack_dequantize out")
+        if y.dtype not in _TORCH_TAG:
+            raise ValueError(f"unpack_dequantize out: unsupported dtype {y.dtype}")
     _check("gact_unpack_dequantize", lib().gact_unpack_dequantize(
         packed.data_ptr(), group_min.data_ptr(), group_scale.data_ptr(), n, group_size, bits,
         y.data_ptr(), _TORCH_TAG[y.dtype], _stream(packed)))
@@ -206,6 +245,8 @@ def quantize_pack_batch(xs: Sequence[torch.Tensor], bits: Sequence[int], seeds: 
         _require_cuda(x)
         if not x.is_contiguous():
             raise ValueError("quantize_pack_batch needs contiguous tensors")
+        if x.device != xs[0].device:
+            raise ValueError("quantize_pack_batch: all tensors on one device")
         n = x.numel()
         if outs is None:
             packed = torch.empty(max(packed_words(n, b), 0), dtype=torch.int32, device=x.device)
@@ -213,6 +254,7 @@ def quantize_pack_batch(xs: Sequence[torch.Tensor], bits: Sequence[int], seeds: 
             sc = torch.empty_like(mn)
         else:
             packed, mn, sc = outs[i]
+            _codes_need(packed, mn, sc, n, b, group_size, x.device, f"quantize_pack_batch outs[{i}]")
         rows.append((x.data_ptr(), packed.data_ptr(), mn.data_ptr(), sc.data_ptr(), n,
                      s & (2**64 - 1), b, _TORCH_TAG[x.dtype]))
         res.append(CompressedTensor(packed, mn, sc, tuple(x.shape), x.dtype, b, group_size, s))
@@ -229,7 +271,14 @@ def unpack_dequantize_batch(cts: Sequence[CompressedTensor], outs: Sequence[torc
     if len(gs) > 1:
         raise ValueError("one group size per batch")
     for i, c in enumerate(cts):
-        y = torch.empty(c.shape, dtype=c.dtype, device=c.packed.device) if outs is None else outs[i]
+        _require_cuda(c.packed, c.group_min, c.group_scale)
+        _codes_need(c.packed, c.group_min, c.group_scale, c.numel, c.bits, c.group_size, cts[0].packed.device,
+                    f"unpack_dequantize_batch[{i}]")
+        if outs is None:
+            y = torch.empty(c.shape, dtype=c.dtype, device=c.packed.device)
+        else:
+            y = outs[i]
+            _need(y, c.numel, None, cts[0].packed.device, f"unpack_dequantize_batch outs[{i}]")
         rows.append((y.data_ptr(), c.packed.data_ptr(), c.group_min.data_ptr(),
                      c.group_scale.data_ptr(), c.numel, 0, c.bits, _TORCH_TAG[y.dtype]))
         ys.append(y)
@@ -334,9 +383,12 @@ def allocate_bits(sensitivity, numel, budget_bits: int, ladder: Sequence[int] = 
     return out[:c.size]
 
 
-def S(b: int) -> float:
-    """S(b) = (2^b - 1)^-2 of P:479-480; S(32) = 0 (uncompressed)."""
-    return 0.0 if b == 32 else 1.0 / float((1 << b) - 1) ** 2
+def variance_factor(bits: int) -> float:
+    """S(b) of P:479-480 (S(32) = 0): gact_variance_factor, the allocator's own definition."""
+    v = float(lib().gact_variance_factor(int(bits)))
+    if v < 0:
+        raise ValueError(f"no variance factor for {bits} bits")
+    return v
 
 
 def sq_diff_sum(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
@@ -372,6 +424,8 @@ class BatchPlan:
         self.table = np.zeros(len(xs), dtype=_DESC_NP)
         for i, (x, (p, mn, sc), b) in enumerate(zip(xs, outs, bits)):
             _require_cuda(x, p, mn, sc)
+            _need(x, x.numel(), None, xs[0].device, f"BatchPlan xs[{i}]")
+            _codes_need(p, mn, sc, x.numel(), int(b), group_size, xs[0].device, f"BatchPlan outs[{i}]")
             self.table[i] = (x.data_ptr(), p.data_ptr(), mn.data_ptr(), sc.data_ptr(), x.numel(), 0, int(b),
                              _TORCH_TAG[x.dtype])
         self.stream_of = xs[0] if len(xs) else None

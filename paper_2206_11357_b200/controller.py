@@ -45,6 +45,7 @@ import numpy as np
 import torch
 
 from . import dist as gdist
+from . import variance_factor
 
 SUPPORTED = (torch.float32, torch.bfloat16, torch.float16)
 LADDER = (1, 2, 4, 8, 32)
@@ -251,8 +252,12 @@ class Controller:
     def _params(self):
         return [p for p in self.model.parameters() if p.requires_grad]
 
-    def _run(self, fwdbwdprop) -> torch.Tensor:
-        """One fwd+bwd under compression; returns the flattened fp32 gradient."""
+    def _run(self, fwdbwdprop, rng=None) -> torch.Tensor:
+        """One fwd+bwd under compression; returns the flattened fp32 gradient. `rng` (a
+        snapshot from _rng_snapshot) is restored first, so that every pass of Alg. 1 draws
+        the same dropout masks / stochastic-layer noise."""
+        if rng is not None:
+            self._rng_restore(rng)
         for p in self._params():
             p.grad = None
         with self.hooks():
@@ -261,6 +266,18 @@ class Controller:
         grads = [p.grad.reshape(-1).float() for p in self._params() if p.grad is not None]
         return torch.cat(grads) if grads else torch.zeros(0)
 
+    @staticmethod
+    def _rng_snapshot():
+        cuda = torch.cuda.get_rng_state_all() if torch.cuda.is_available() else None
+        return torch.get_rng_state(), cuda
+
+    @staticmethod
+    def _rng_restore(snap):
+        cpu, cuda = snap
+        torch.set_rng_state(cpu)
+        if cuda is not None:
+            torch.cuda.set_rng_state_all(cuda)
+
     # ---------------------------------------------------------------- Alg. 1
     def estimate_sensitivity(self, fwdbwdprop, repeats: int = 1) -> np.ndarray:
         """Alg. 1: c_l = 1/2 ||g0 - g1||^2 / S(b_l), where g0 seeds every Q^(l)
@@ -268,28 +285,33 @@ class Controller:
         every slot at est_bits (Alg. 1 accepts any scheme b; under the linearisation c_l does
         not depend on b). Averaged over `repeats` seed draws."""
         saved_params = [p.grad for p in self._params()]
+        # Alg. 1 fixes every source of randomness except Q^(l) (P:516-521): all passes start
+        # from one snapshot of the torch generators (dropout masks identical in g0 and g1).
+        rng = self._rng_snapshot()
         L = len(self.numel)
         if L == 0:  # discover the slots with one pass
             self._bits_override = lambda s: self.est_bits
-            self._run(fwdbwdprop)
+            self._run(fwdbwdprop, rng)
             self._bits_override = None
             L = len(self.numel)
         c = np.zeros(L)
         b_est = self.est_bits
+        s_est = variance_factor(b_est)
         self._bits_override = lambda s: b_est
         try:
             for rep in range(repeats):
                 base = _splitmix64(self.seed ^ 0xA5A5A5A5 ^ (self.iteration << 20) ^ rep)
                 r = [_splitmix64(base + l + 1) for l in range(L + 1)]        # r_1 .. r_{L+1}
                 self._seed_of = lambda s: r[s] if s < L else r[L]
-                g0 = self._run(fwdbwdprop)
+                g0 = self._run(fwdbwdprop, rng)
                 for l in range(L):
                     self._seed_of = (lambda s, l=l: r[L] if s == l else (r[s] if s < L else r[L]))
-                    g1 = self._run(fwdbwdprop)
-                    c[l] += 0.5 * self.backend.sq_diff(g0, g1) / (1.0 / float((1 << b_est) - 1) ** 2)
+                    g1 = self._run(fwdbwdprop, rng)
+                    c[l] += 0.5 * self.backend.sq_diff(g0, g1) / s_est
         finally:
             self._seed_of = None
             self._bits_override = None
+            self._rng_restore(rng)
             for p, g in zip(self._params(), saved_params):
                 p.grad = g
         return c / repeats
@@ -317,8 +339,7 @@ class Controller:
         """V(b) <= sum_l c_l S(b_l) (eqn:var-decomposition)."""
         if self.sensitivity is None or not self.bits:
             return float("nan")
-        return float(sum(c * (0.0 if b == RAW else 1.0 / float((1 << b) - 1) ** 2)
-                         for c, b in zip(self.sensitivity, self.bits)))
+        return float(sum(c * variance_factor(b) for c, b in zip(self.sensitivity, self.bits)))
 
     # ---------------------------------------------------------------- training iteration
     def iterate(self, fwdbwdprop):

@@ -299,6 +299,11 @@ static double S_of(int32_t b) {
   return 1.0 / (m * m);
 }
 
+extern "C" double gact_variance_factor(int32_t bits) {
+  if (bits == 32 || (bits >= 1 && bits <= 16)) return S_of(bits);
+  return -1.0;
+}
+
 gact_status gact_allocate_bits(const double* c, const int64_t* D, int32_t L,
                                const int32_t* ladder, int32_t n_ladder, uint64_t budget_bits,
                                int32_t* bits_out) {

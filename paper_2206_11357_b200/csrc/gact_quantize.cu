@@ -330,7 +330,10 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
   const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
   const int64_t cunits = P.tiles_total / U;   // a quantize tile is one group here
   int cur = 0, par = 0;
-  for (int64_t cu = blockIdx.x; cu < cunits; cu += gridDim.x, par ^= 1) {
+  // `par` selects the half of red[] a unit uses. It flips only on units that pass the
+  // barrier: a guarded unit (no barrier) between two full units must not flip it, or the
+  // second full unit would write the half the first one's warps may still be reading.
+  for (int64_t cu = blockIdx.x; cu < cunits; cu += gridDim.x) {
     cur = advance_cursor(P, cur, cu * U);
     const QTensor& T = P.t[cur];
     const int64_t e_unit = (cu * U - P.tile_start[cur]) * TE;
@@ -373,6 +376,7 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
       mnk[k] = warp_min(red[par][k][0][lane & (kWarps - 1)]);
       mxk[k] = warp_max(red[par][k][1][lane & (kWarps - 1)]);
     }
+    par ^= 1;
     const int sel = lane & (U - 1);
     float a = mnk[0], b = mxk[0];
 #pragma unroll

@@ -15,26 +15,37 @@ import torch
 import torch.distributed as dist
 
 
-def _active() -> bool:
-    return dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+def _active(force: bool = False) -> bool:
+    if not (dist.is_available() and dist.is_initialized()):
+        return False
+    return force or dist.get_world_size() > 1
 
 
 _side_streams: dict = {}
 
 
-def merge_sensitivities(c_local, device=None) -> np.ndarray:
+def _side_stream(device) -> torch.cuda.Stream:
+    """The exchange's stream on `device`: highest priority, so that the all-reduce kernel is
+    scheduled ahead of queued compression CTAs as soon as SMs free up."""
+    side = _side_streams.get(device)
+    if side is None:
+        lo, hi = torch.cuda.Stream.priority_range()
+        side = _side_streams[device] = torch.cuda.Stream(device, priority=min(lo, hi))
+    return side
+
+
+def merge_sensitivities(c_local, device=None, force: bool = False) -> np.ndarray:
     """All-reduce(SUM) / world of the local sensitivity vector (float64, L entries).
 
-    With NCCL the exchange runs on a dedicated side stream, so that waiting for the merged
-    vector (the allocator runs on the host) does not wait for the compute stream's queue."""
+    With NCCL the exchange runs on a dedicated high-priority side stream, so that waiting for
+    the merged vector (the allocator runs on the host) waits only for the exchange, not for the
+    compute stream's queue. `force` runs the exchange in a one-rank group too (tests)."""
     c = np.ascontiguousarray(c_local, dtype=np.float64)
-    if not _active():
+    if not _active(force):
         return c
     backend = dist.get_backend()
     if backend == "nccl" and device is not None:
-        side = _side_streams.get(device)
-        if side is None:
-            side = _side_streams[device] = torch.cuda.Stream(device)
+        side = _side_stream(device)
         with torch.cuda.stream(side):
             t = torch.from_numpy(c).to(device, non_blocking=False)
             dist.all_reduce(t, op=dist.ReduceOp.SUM)

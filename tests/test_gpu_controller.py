@@ -296,3 +296,47 @@ def test_resnet18_context(ctl):
         assert c.stats.packed > 20 and c.stats.raw > 0
         assert c.compression_ratio() > (32 / (b + 0.25)) * 0.9
     assert err[8] < err[4] and cos[8] > 0.97 and cos[4] > 0.5, (err, cos)
+
+
+def test_alg1_fixes_dropout_noise(ctl):
+    """Alg. 1 fixes every source of randomness except Q^(l): with dropout in the
+    model, two passes with the same compressor seeds give bit-identical gradients, so
+    ||g0 - g1||^2 holds compression noise only, and the estimate is reproducible."""
+    torch.manual_seed(3)
+    m = torch.nn.Sequential(torch.nn.Linear(64, 256), torch.nn.ReLU(), torch.nn.Dropout(0.5),
+                            torch.nn.Linear(256, 10)).cuda()
+    x, y = torch.randn(256, 64, device="cuda"), torch.randint(0, 10, (256,), device="cuda")
+    c = ctl.Controller(m, avg_bits=4, merge=False, adapt_interval=10**9)
+    f = fwdbwd(m, x, y)
+    c1 = c.estimate_sensitivity(f)
+    c2 = c.estimate_sensitivity(f)
+    assert np.array_equal(c1, c2)
+    rng = c._rng_snapshot()
+    c._seed_of = lambda s: 1000 + s
+    g0 = c._run(f, rng)
+    g0b = c._run(f, rng)
+    c._seed_of = None
+    assert torch.equal(g0, g0b)
+
+
+def test_controller_offset_views(ctl):
+    """Saved tensors that are views with a storage offset breaking 16-byte alignment (x[1:])
+    are compressed (the binding copies them once) instead of failing with ALIGNMENT."""
+    import paper_2206_11357_b200 as gact
+    base = torch.randn(4097, 64, device="cuda")
+    v = base[1:]  # offset 64 floats: aligned; a 1-element offset is not
+    w = base.view(-1)[1:1 + 4096 * 63]
+    for t in (v, w):
+        ct = gact.quantize_pack(t, 4, 5)
+        ref = gact.quantize_pack(t.clone(), 4, 5)
+        assert torch.equal(ct.packed, ref.packed) and torch.equal(ct.group_min, ref.group_min)
+    torch.manual_seed(0)
+    lin = torch.nn.Linear(63, 10).cuda()
+    xb = torch.randn(300 * 63 + 1, device="cuda", requires_grad=True)
+
+    def f():
+        lin(xb[1:].view(300, 63)).square().sum().backward()
+    c = ctl.Controller(lin, avg_bits=4, merge=False, adapt_interval=10**9, min_numel=1)
+    c.iteration = 1
+    c.iterate(f)
+    assert c.stats.packed >= 1 and torch.isfinite(lin.weight.grad).all()

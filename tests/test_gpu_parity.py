@@ -199,7 +199,7 @@ def test_determinism_and_streams(gact):
     assert not torch.equal(a.packed, c.packed)
 
 
-@pytest.mark.parametrize("G", [64, 256, 1024])
+@pytest.mark.parametrize("G", GROUPS)
 def test_batch_equals_single(gact, G):
     """Batched launches (mixed dtypes and bits, > GACT_MAX_BATCH tensors) give results
     identical to one call per tensor."""
@@ -220,6 +220,34 @@ def test_batch_equals_single(gact, G):
         assert torch.equal(ct.group_min, single.group_min)
         assert torch.equal(ct.group_scale, single.group_scale)
         assert torch.equal(y.view(-1), single.decompress().view(-1))
+
+
+@pytest.mark.parametrize("dtype", DTYPES, ids=["f32", "bf16", "f16"])
+@pytest.mark.parametrize("G", [2048, 4096])
+def test_batch_large_groups_vs_oracle(gact, orc, dtype, G):
+    """Batched launches at G = 2048 / 4096 (the fp32 CTA-wide kernel, the 2-byte register
+    and shared-memory-stage kernels) against the oracle, tensor by tensor. 40 ragged tensors
+    per launch: every tensor ends in a partial group and is padded to 64 tiles, so guarded
+    units interleave with full ones inside one CTA's sequence, and the launch has more units
+    than its grid (CTAs wrap across tensor tails)."""
+    rng = np.random.default_rng(G + TAGS[dtype])
+    xs, bits, seeds = [], [], []
+    for i in range(40):
+        n = int(rng.integers(2 * G, 48 * G)) + int(rng.integers(1, G))
+        xs.append(make_input(n, dtype, seed=1000 + i))
+        bits.append(BITS[i % 4])
+        seeds.append(synth.tensor_seed(29, i))
+    batch = gact.quantize_pack_batch(xs, bits, seeds, G)
+    ys = gact.unpack_dequantize_batch(batch)
+    torch.cuda.synchronize()
+    for x, b, s, ct, y in zip(xs, bits, seeds, batch, ys):
+        ref_p, ref_mn, ref_sc = orc.quantize_pack(oracle_input(x), TAGS[dtype], G, b, s)
+        assert np.array_equal(host_bits(ct.packed), ref_p)
+        assert np.array_equal(host_bits(ct.group_min), ref_mn.view(np.uint32))
+        assert np.array_equal(host_bits(ct.group_scale), ref_sc.view(np.uint32))
+        ref_y = orc.unpack_dequantize(ref_p, ref_mn, ref_sc, x.numel(), G, b, TAGS[dtype])
+        d = ulp_distance(host_bits(y), ref_y, 32 if dtype == torch.float32 else 16)
+        assert d.max(initial=0) <= 1
 
 
 def test_unbiased_on_gpu(gact, orc):
@@ -372,3 +400,25 @@ def test_philox_blocks_at_counter_boundaries(gact, orc, shared, nblk):
                 b = (blk + 32 * m) % 2**64
                 ref = orc.philox4x32_10([b & 0xFFFFFFFF, b >> 32, 0, 0], [seed & 0xFFFFFFFF, seed >> 32])
                 assert np.array_equal(got[4 * m: 4 * m + 4], ref), (hex(blk), m, hex(seed))
+
+
+def test_binding_rejects_bad_buffers(gact):
+    """Caller-supplied outputs are checked before any launch (size, dtype, device,
+    contiguity): a short or strided buffer raises instead of being written out of bounds."""
+    x = make_input(10000, torch.bfloat16, seed=1)
+    ct = gact.quantize_pack(x, 4, 1)
+    short = torch.empty(ct.packed.numel() - 1, dtype=torch.int32, device="cuda")
+    with pytest.raises(ValueError):
+        gact.quantize_pack(x, 4, 1, out=(short, ct.group_min, ct.group_scale))
+    with pytest.raises(ValueError):
+        gact.quantize_pack(x, 4, 1, out=(ct.packed, ct.group_min.double(), ct.group_scale))
+    with pytest.raises(ValueError):
+        gact.unpack_dequantize(ct.packed, ct.group_min, ct.group_scale, 10000, 4,
+                               out=torch.empty(9999, dtype=torch.bfloat16, device="cuda"))
+    with pytest.raises(ValueError):
+        gact.unpack_dequantize(ct.packed, ct.group_min, ct.group_scale, 10000, 4,
+                               out=torch.empty(20000, dtype=torch.float32, device="cuda")[::2])
+    with pytest.raises(ValueError):  # codes too short for n
+        gact.unpack_dequantize(ct.packed[:-1], ct.group_min, ct.group_scale, 10000, 4)
+    y = gact.unpack_dequantize(ct.packed, ct.group_min, ct.group_scale, 10000, 4, dtype=torch.bfloat16)
+    assert torch.equal(y, ct.decompress())
