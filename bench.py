@@ -100,15 +100,19 @@ def measured_peak():
 
 
 class ClockSampler:
-    """SM clocks and throttle reasons sampled DURING the timed region (NVML, every 5 ms, in a
-    thread started before the region; nvidia-smi as a fallback)."""
+    """SM clocks and throttle reasons sampled DURING the timed region (NVML every 1 ms in a
+    thread started before the region, plus one synchronous sample taken after the region's
+    work is enqueued and before the host waits for it, so that regions shorter than the poll
+    interval -- the 256 MiB configs[1] steps -- are sampled too)."""
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                0x4: "sw_power_cap"}
+    PERIOD_S = 0.001
 
     def __init__(self, index: int):
         self.index, self.rows, self.stop = index, [], threading.Event()
         self.active = threading.Event()
         self.max_mhz = None
+        self._read = None
 
     def __enter__(self):
         try:
@@ -117,18 +121,29 @@ class ClockSampler:
             h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
 
+            def read():
+                return (pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                        pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))
+            self._read = read
+
             def poll():
                 while not self.stop.is_set():
                     if self.active.is_set():
-                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                        self.rows.append((sm, rs))
-                    time.sleep(0.005)
+                        self.rows.append(read())
+                    time.sleep(self.PERIOD_S)
             self.thread = threading.Thread(target=poll, daemon=True)
             self.thread.start()
         except Exception:
             self.thread = None
         return self
+
+    def sample_now(self):
+        """One synchronous sample (call while the timed work is still executing)."""
+        if self._read is not None and self.active.is_set():
+            try:
+                self.rows.append(self._read())
+            except Exception:
+                pass
 
     def start(self):
         self.active.set()
@@ -147,7 +162,7 @@ class ClockSampler:
         sm = [r[0] for r in self.rows]
         reasons = sorted({name for _, rs in self.rows for bit, name in self.REASONS.items() if rs & bit})
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "reasons": reasons,
-                "samples": len(self.rows), "source": "nvml, 5 ms, timed region only"}
+                "samples": len(self.rows), "source": "nvml, 1 ms + one sample after enqueue, timed region only"}
 
 
 # ------------------------------------------------------------------------- our arm
@@ -255,6 +270,7 @@ def run_ours(args):
         for it in range(args.steps):
             bits = step(args.warmup + it, ev[it])
         t1.record(stream)
+        clk.sample_now()  # the enqueued steps are still running
         torch.cuda.synchronize()
         clk.end()
     if world > 1:

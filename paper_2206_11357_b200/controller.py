@@ -28,7 +28,8 @@ the libgact C ABI.
   copy of slot l - 1 (the next one backward needs) on a swap-in stream, and CUDA events
   order the streams.
 * Failure alert: the predicted compression variance V = sum_l c_l S(b_l) is
-  compared with the running variance of the gradient; a warning is raised when V dominates.
+  compared with the running variance of the gradient; a warning is raised when V is more
+  than alert_ratio (default 1/2) of it, i.e. when compression dominates the gradient noise.
 
 Slots are identified by the order in which distinct context tensors are first saved in an
 iteration (a static graph saves the same tensors in the same order every iteration).
@@ -128,12 +129,13 @@ class Stats:
     bytes_raw: int = 0       # bytes the compressed tensors would have taken
     bytes_compressed: int = 0
     alerts: list = field(default_factory=list)
+    variance_log: list = field(default_factory=list)  # (iteration, V(b), Var[g_hat]) per iteration
 
 
 class Controller:
     def __init__(self, model: torch.nn.Module, avg_bits: float = 4.0, group_size: int = 256,
                  ladder=LADDER, adapt_interval: int = 100, est_bits: int = 4, seed: int = 0,
-                 min_numel: int = 256, alert_ratio: float = 1.0, backend=None, merge=True,
+                 min_numel: int = 256, alert_ratio: float = 0.5, backend=None, merge=True,
                  swap: bool = False):
         self.model = model
         self.avg_bits = float(avg_bits)
@@ -157,6 +159,8 @@ class Controller:
         self._bits_override = None       # slot -> bits override (Alg. 1 estimation scheme)
         self._grad_mean = None
         self._grad_sq = None
+        self._grad_count = 0
+        self._grad_w2 = 1.0
         self.swap = swap
         self._swapped: dict = {}         # slot -> SwappedTensor (this iteration)
         self._pending: list = []         # (event, device tensors) of swap-outs in flight
@@ -355,22 +359,44 @@ class Controller:
         self._track_variance()
         self.iteration += 1
 
+    def gradient_variance(self) -> float:
+        """Var[g_hat] summed over coordinates, from the running (exponentially weighted) mean
+        and second moment of the AC gradient over iterations ("maintaining a running
+        mean of the gradient"), with the weights' bias correction: for weights w_t summing to
+        1, E[sum_t w_t g_t^2 - (sum_t w_t g_t)^2] = (1 - sum_t w_t^2) Var[g]."""
+        if self._grad_mean is None or self._grad_count < 2:
+            return float("nan")
+        raw = float((self._grad_sq - self._grad_mean ** 2).clamp_(min=0).sum().item())
+        return raw / max(1e-12, 1.0 - self._grad_w2)
+
     def _track_variance(self, momentum: float = 0.9):
-        """Running mean / second moment of the gradient; alert when the predicted
-        compression variance dominates the gradient variance."""
+        """Running mean / second moment of the gradient; alert when the predicted compression
+        variance V(b) = sum_l c_l S(b_l) is a large share of the gradient variance Var[g_hat]
+        (P:536-537). Var[g_hat] includes the compression noise itself, so V / Var[g_hat] <= 1
+        when c is accurate, and the default threshold alert_ratio = 0.5 reads "compression is
+        the larger part of the gradient noise". No alert before 1 / (1 - momentum) tracked
+        iterations (the running estimate needs that many samples)."""
         grads = [p.grad.reshape(-1).float() for p in self._params() if p.grad is not None]
         if not grads:
             return
         g = torch.cat(grads)
+        a = 1.0 - momentum
         if self._grad_mean is None:
             self._grad_mean, self._grad_sq = g.clone(), (g * g)
+            self._grad_count, self._grad_w2 = 1, 1.0
             return
-        self._grad_mean.mul_(momentum).add_(g, alpha=1 - momentum)
-        self._grad_sq.mul_(momentum).add_(g * g, alpha=1 - momentum)
-        var = float((self._grad_sq - self._grad_mean ** 2).clamp_(min=0).sum().item())
+        self._grad_mean.mul_(momentum).add_(g, alpha=a)
+        self._grad_sq.mul_(momentum).add_(g * g, alpha=a)
+        self._grad_count += 1
+        self._grad_w2 = momentum * momentum * self._grad_w2 + a * a
+        var = self.gradient_variance()
         V = self.predicted_variance()
+        self.stats.variance_log.append((self.iteration, V, var))
+        if self._grad_count < round(1.0 / a):
+            return
         if var > 0 and not math.isnan(V) and V / var > self.alert_ratio:
-            msg = f"GACT: predicted compression variance {V:.3g} exceeds {self.alert_ratio} x gradient variance {var:.3g}; raise the bit budget"
+            msg = (f"GACT: predicted compression variance {V:.3g} is more than {self.alert_ratio} x the "
+                   f"gradient variance {var:.3g}; raise the bit budget")
             self.stats.alerts.append((self.iteration, V, var))
             warnings.warn(msg, RuntimeWarning, stacklevel=3)
 

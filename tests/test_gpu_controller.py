@@ -163,16 +163,104 @@ def test_dedup_and_ratio(ctl):
     assert c.compression_ratio() >= 6.0
 
 
+def _linear_closed_form(orc, h, R, bits, G=256):
+    """Alg. 1's c for out = h W^T with loss <out, R> (one compressed context tensor h,
+    grad W = R^T h, linear in h): E||g0 - g1||^2 = 2 sum_{i,j} Var_Q[(R^T Q(h))_{ij}] with
+    Var_Q[Q(h)_{bj}] = p (1 - p) scale^2 per element (independent elements, B1/B2 P:477-480),
+    p = frac(T), T = (h - mn) / scale from the oracle's group statistics (p agrees with the
+    generator's exact probability to 2^-17). Returns (c, sigma of one Alg. 1 estimate): the
+    estimate's variance 2 sum_j tr(C_j^2) / (2 S)^2 with C_j = R^T diag(2 v_.j) R."""
+    hh = h.detach().cpu().numpy().astype(np.float32)
+    mn, sc = orc.group_stats(hh.reshape(-1), orc.F32, G, bits)
+    mn = np.repeat(mn.astype(np.float64), G)[: hh.size].reshape(hh.shape)
+    sc = np.repeat(sc.astype(np.float64), G)[: hh.size].reshape(hh.shape)
+    T = np.where(sc > 0, (hh.astype(np.float64) - mn) / np.where(sc > 0, sc, 1), 0.0)
+    p = T - np.floor(T)
+    v = p * (1 - p) * sc * sc                         # [B, K]
+    Rn = R.detach().cpu().numpy().astype(np.float64)  # [B, O]
+    S = orc.S(bits)
+    c = float(((Rn * Rn).sum(1)[:, None] * v).sum()) / S
+    var_sq = 0.0
+    for j in range(v.shape[1]):
+        C = Rn.T @ (2 * v[:, j:j + 1] * Rn)           # covariance of (g0 - g1)_{., j}
+        var_sq += 2 * float(np.sum(C * C))
+    return c, np.sqrt(var_sq) / (2 * S)
+
+
+@pytest.mark.parametrize("est_bits", [2, 4, 8])
+def test_alg1_closed_form_linear(ctl, orc, est_bits):
+    """Alg. 1 pinned to a closed form: for a linear layer the controller's c
+    (averaged over 24 independent seed draws) equals the exact compression variance of the
+    weight gradient / S(b) within 5 standard deviations of the estimator."""
+    torch.manual_seed(11)
+    lin = torch.nn.Linear(512, 16, bias=False).cuda()
+    h = torch.randn(256, 512, device="cuda").mul_(torch.rand(256, 1, device="cuda") * 3).requires_grad_(True)
+    R = torch.randn(256, 16, device="cuda")
+
+    def f():
+        (lin(h) * R).sum().backward()
+    c = ctl.Controller(lin, merge=False, adapt_interval=10**9, est_bits=est_bits, seed=7, min_numel=1)
+    reps = 24
+    est = c.estimate_sensitivity(f, repeats=reps)
+    assert len(c.numel) == 1 and c.numel[0] == h.numel()   # the one context tensor: h
+    exact, sigma = _linear_closed_form(orc, h, R, est_bits)
+    assert abs(est[0] - exact) <= 5 * sigma / np.sqrt(reps), (est[0], exact, sigma)
+    assert sigma / np.sqrt(reps) < 0.02 * exact              # the pin is tight (< 2% per sigma)
+
+
+def test_alert_calibrated_linear(ctl, orc):
+    """When compression is the only gradient noise (fixed batch, fixed weights), the running
+    gradient variance estimate Var[g_hat] and the predicted V(b) = sum_l c_l S(b_l) agree
+    (ratio ~ 1), so the default threshold (1/2) fires."""
+    torch.manual_seed(12)
+    lin = torch.nn.Linear(512, 16, bias=False).cuda()
+    h = torch.randn(256, 512, device="cuda").requires_grad_(True)
+    R = torch.randn(256, 16, device="cuda")
+
+    def f():
+        (lin(h) * R).sum().backward()
+    c = ctl.Controller(lin, avg_bits=2, ladder=(2,), merge=False, adapt_interval=10**9, seed=3, min_numel=1)
+    with pytest.warns(RuntimeWarning):
+        for _ in range(60):
+            c.iterate(f)
+    ratios = [V / var for (_, V, var) in c.stats.variance_log[20:]]
+    assert 0.7 < float(np.median(ratios)) < 1.4, ratios
+    exact, _ = _linear_closed_form(orc, h, R, 2)
+    assert abs(c.predicted_variance() / (exact * orc.S(2)) - 1) < 0.25
+
+
 def test_failure_alert(ctl):
-    """at a 1-bit budget with a tiny batch, the predicted compression variance
-    dominates the gradient variance and the controller warns."""
+    """P:536-537 at the default threshold: a 1-bit budget with a tiny batch warns (compression
+    dominates the gradient noise)."""
     m = mlp([16, 256, 256, 4], seed=1)
     x, y = torch.randn(64, 16, device="cuda"), torch.randint(0, 4, (64,), device="cuda")
-    c = ctl.Controller(m, avg_bits=1, ladder=(1, 2), merge=False, adapt_interval=10**9, alert_ratio=1e-6)
+    c = ctl.Controller(m, avg_bits=1, ladder=(1,), merge=False, adapt_interval=10**9)
+    assert c.alert_ratio == 0.5
     with pytest.warns(RuntimeWarning):
-        for _ in range(4):
+        for _ in range(16):
             c.iterate(fwdbwd(m, x, y))
     assert c.stats.alerts
+
+
+def test_no_alert_at_8_bits_training(ctl):
+    """...and stays silent at 8 bits on the convergence task (fresh minibatches, SGD steps),
+    where compression noise is a small part of the gradient noise."""
+    import warnings
+    g = torch.Generator(device="cuda").manual_seed(0)
+    centers = torch.randn(16, 64, device="cuda", generator=g) * 1.5
+    m = mlp([64, 512, 512, 16], act=torch.nn.ReLU, seed=1)
+    opt = torch.optim.SGD(m.parameters(), lr=0.05, momentum=0.9)
+    c = ctl.Controller(m, avg_bits=8, ladder=(8,), merge=False, adapt_interval=50, seed=3)
+    with warnings.catch_warnings():
+        warnings.simplefilter("error", RuntimeWarning)
+        for it in range(120):
+            y = torch.randint(0, 16, (512,), device="cuda", generator=g)
+            x = centers[y] + torch.randn(512, 64, device="cuda", generator=g)
+            c.iterate(fwdbwd(m, x, y))
+            opt.step()
+    assert not c.stats.alerts
+    ratios = [V / var for (_, V, var) in c.stats.variance_log[10:] if var > 0]
+    assert max(ratios) < c.alert_ratio and float(np.median(ratios)) < 0.1, ratios
 
 
 def test_swap_prefetch_same_gradients_less_memory(ctl):
@@ -237,6 +325,70 @@ def test_checkpoint_segments_cb1(ctl):
     g = torch.cat([p.grad.reshape(-1) for p in model.parameters()])
     assert c.stats.packed > 0 and torch.isfinite(g).all()
     assert float((g - ref).norm() / ref.norm()) < 0.2
+
+
+class _RecordingBackend:
+    """The libgact backend, recording each compression (input copy, bits, seed, result)."""
+
+    def __init__(self, group_size=256):
+        from paper_2206_11357_b200.controller import LibgactBackend
+        self.inner = LibgactBackend(group_size)
+        self.calls = []
+        self.phase = "forward"
+
+    def compress(self, t, bits, seed):
+        ct = self.inner.compress(t, bits, seed)
+        self.calls.append((self.phase, t.detach().clone(), bits, seed, ct))
+        return ct
+
+    def decompress(self, h):
+        return self.inner.decompress(h)
+
+    def nbytes(self, h):
+        return self.inner.nbytes(h)
+
+    def sq_diff(self, a, b):
+        return self.inner.sq_diff(a, b)
+
+
+def test_checkpoint_cb1_codes_match_oracle(ctl, orc):
+    """CB1 against the oracle: every tensor the controller compresses under
+    checkpoint segments -- the segment inputs saved in forward and the activations re-saved
+    while backward recomputes the segments -- is compressed with the slot's bits and seed,
+    and its codes, group min and scale equal the oracle's for that input, bits and seed."""
+    from torch.utils.checkpoint import checkpoint
+    torch.manual_seed(0)
+    blocks = torch.nn.ModuleList([torch.nn.Sequential(torch.nn.Linear(256, 256), torch.nn.Tanh())
+                                  for _ in range(3)]).cuda()
+    head = torch.nn.Linear(256, 8).cuda()
+    model = torch.nn.ModuleList([blocks, head])
+    x, y = torch.randn(512, 256, device="cuda"), torch.randint(0, 8, (512,), device="cuda")
+    rec = _RecordingBackend()
+
+    def f():
+        rec.phase = "forward"
+        h = x
+        for b in blocks:
+            h = checkpoint(b, h, use_reentrant=False)
+        loss = torch.nn.functional.cross_entropy(head(h), y)
+        rec.phase = "backward"
+        loss.backward()
+    c = ctl.Controller(model, avg_bits=4, ladder=(2, 4, 8), merge=False, adapt_interval=10**9, backend=rec,
+                       min_numel=1)
+    c.bits = [2, 4, 8] * 8
+    c.iteration = 1
+    c.iterate(f)
+    phases = [ph for ph, *_ in rec.calls]
+    assert phases.count("forward") >= 1 and phases.count("backward") >= 1, phases
+    torch.cuda.synchronize()
+    c.iteration -= 1  # the seeds of the iteration just run
+    for slot, (ph, t, bits, seed, ct) in enumerate(rec.calls):
+        assert bits == c.bits[slot] and seed == c._slot_seed(slot)
+        xh = t.contiguous().cpu().numpy().reshape(-1)
+        p, mn, sc = orc.quantize_pack(xh, orc.F32, 256, bits, seed)
+        assert np.array_equal(ct.packed.cpu().numpy().view(np.uint32), p), (slot, ph)
+        assert np.array_equal(ct.group_min.cpu().numpy(), mn)
+        assert np.array_equal(ct.group_scale.cpu().numpy(), sc)
 
 
 def test_training_converges_like_fp32(ctl):

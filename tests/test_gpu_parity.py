@@ -80,10 +80,16 @@ def check_dequantize(gact, orc, ct, ref, n, G, bits, dtype):
     ref_y = orc.unpack_dequantize(ref_p, ref_mn, ref_sc, n, G, bits, TAGS[dtype])
     d = ulp_distance(host_bits(y), ref_y, 32 if dtype == torch.float32 else 16)
     assert d.max(initial=0) <= 1, f"max ulp distance {d.max()}"
+    c = DEQUANT_COUNTS.setdefault(str(dtype).replace("torch.", ""), [0, 0])
+    c[0] += int((d != 0).sum())
+    c[1] += int(d.size)
     return int((d != 0).sum())
 
 
-def make_input(n, dtype, seed, kind="normal"):
+DEQUANT_COUNTS = {}  # output dtype -> [values differing from the oracle (by 1 ulp), values checked]
+
+
+def make_input(n, dtype, seed, kind="normal", group=256):
     rng = np.random.default_rng(seed)
     v = rng.standard_normal(n) * 10.0 ** rng.uniform(-2, 2)
     if kind == "mixed" and n > 0:
@@ -104,7 +110,55 @@ def make_input(n, dtype, seed, kind="normal"):
             elif r == 5:  # the largest magnitudes the dtype holds without overflow
                 big = 1e4 if dtype == torch.float16 else 1e30
                 v[sl] = rng.standard_normal(v[sl].size) * big
+    if kind == "edge2" and n > 0:
+        return edge_groups(n, dtype, seed, group)
     t = torch.from_numpy(v.astype(np.float32)).to(dtype)
+    return t.cuda()
+
+
+def edge_groups(n, dtype, seed, G):
+    """Groups (of G elements) that exercise the 2-byte paths at their edges, cycling through:
+    subnormals only (bf16 k 2^-133, f16 k 2^-24; fp32 k 2^-149), subnormals with zeros of
+    both signs, negative zeros only, values just below the largest finite (one sign per
+    group, so that max - min stays finite), the smallest normals with subnormals, mixed signs
+    of tiny magnitude, and a normal group. Values are exact in the dtype (bit patterns)."""
+    rng = np.random.default_rng(seed)
+    if dtype == torch.float32:
+        sub, top, width = 2.0 ** -149, 3.0e38, 32
+    elif dtype == torch.bfloat16:
+        sub, top, width = 2.0 ** -133, 3.38e38, 16
+    else:
+        sub, top, width = 2.0 ** -24, 65504.0, 16
+    nsub = 128 if dtype == torch.bfloat16 else (1024 if dtype == torch.float16 else 1 << 23)
+    v = np.zeros(n, dtype=np.float64)
+    ng = (n + G - 1) // G
+    for g in range(ng):
+        sl = slice(g * G, min(n, (g + 1) * G))
+        m = v[sl].size
+        r = g % 8
+        if r == 0:
+            v[sl] = rng.integers(0, nsub, m) * sub
+        elif r == 1:
+            v[sl] = rng.integers(-nsub + 1, nsub, m) * sub
+            v[sl][rng.random(m) < 0.2] = -0.0
+        elif r == 2:
+            v[sl] = -0.0
+        elif r == 3:
+            v[sl] = top * (1 - rng.random(m) * 0.5)
+        elif r == 4:
+            v[sl] = -top * (1 - rng.random(m) * 0.5)
+        elif r == 5:
+            v[sl] = np.where(rng.random(m) < 0.5, rng.integers(0, nsub, m) * sub, 2.0 ** -126 if width == 32 or dtype == torch.bfloat16 else 2.0 ** -14)
+        elif r == 6:
+            v[sl] = rng.standard_normal(m) * sub * 3
+        else:
+            v[sl] = rng.standard_normal(m)
+    if dtype == torch.float32:
+        t = torch.from_numpy(v.astype(np.float32))
+    elif dtype == torch.float16:
+        t = torch.from_numpy(v.astype(np.float16))
+    else:  # bf16: the subnormal / zero groups are exact; the others are rounded once to bf16
+        t = torch.from_numpy(v.astype(np.float32)).to(torch.bfloat16)
     return t.cuda()
 
 
@@ -130,6 +184,24 @@ def test_quantize_dequantize_parity(gact, orc, dtype, bits, G):
     n = 2 * 8192 + 3 * TE + 8 * 5 + 3
     x = make_input(n, dtype, seed=G * 10 + bits)
     ct, ref = check_quantize(gact, orc, x, G, bits, seed=0xABCDEF0123456789 ^ (G * bits))
+    for ydt in DTYPES:
+        check_dequantize(gact, orc, ct, ref, n, G, bits, ydt)
+
+
+@pytest.mark.parametrize("dtype", DTYPES, ids=["f32", "bf16", "f16"])
+@pytest.mark.parametrize("bits", BITS)
+@pytest.mark.parametrize("G", GROUPS)
+def test_edge_groups_every_kernel(gact, orc, dtype, bits, G):
+    """Subnormal, signed-zero and near-overflow groups through every kernel (all G, every b,
+    every dtype), full units and a ragged tail: codes bit-exact, decoded values <= 1 ulp."""
+    TE = max(G, 256)
+    n = 2 * 8192 + 8 * TE + 77
+    x = make_input(n, dtype, seed=G * 7 + bits, kind="edge2", group=G)
+    hb = host_bits(x)
+    if dtype != torch.float32:  # the inputs really are 2-byte subnormals / -0 / near-max
+        assert np.any((hb & 0x7F80 if dtype == torch.bfloat16 else hb & 0x7C00) == 0)
+        assert np.any(hb == 0x8000)
+    ct, ref = check_quantize(gact, orc, x, G, bits, seed=0x5EED0000 + G + bits)
     for ydt in DTYPES:
         check_dequantize(gact, orc, ct, ref, n, G, bits, ydt)
 
@@ -422,3 +494,17 @@ def test_binding_rejects_bad_buffers(gact):
         gact.unpack_dequantize(ct.packed[:-1], ct.group_min, ct.group_scale, 10000, 4)
     y = gact.unpack_dequantize(ct.packed, ct.group_min, ct.group_scale, 10000, 4, dtype=torch.bfloat16)
     assert torch.equal(y, ct.decompress())
+
+
+def test_zz_report_dequant_mismatch_counts():
+    """Runs last in this file: the dequantize mismatch counts of every check above, per output
+    dtype (written to gpurun_out/dequant_counts.json and quoted in DESIGN.md)."""
+    import json
+    import os
+    if not DEQUANT_COUNTS:
+        pytest.skip("no dequantize check ran")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    os.makedirs(os.path.join(root, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(root, "gpurun_out", "dequant_counts.json"), "w") as f:
+        json.dump(DEQUANT_COUNTS, f)
+    print("dequantize mismatches (1 ulp) / values:", DEQUANT_COUNTS)
