@@ -44,7 +44,7 @@ def lib() -> ctypes.CDLL:
         i32, i64, u64, u32 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint32
         sig = {
             "oracle_philox4x32_10": (None, [P, P, P]),
-            "oracle_lane16": (u32, [u64, u64]),
+            "oracle_rand8": (u32, [u64, u64]),
             "oracle_widen": (ctypes.c_float, [P, i32, i64]),
             "oracle_round_to_dtype": (u32, [ctypes.c_double, i32]),
             "oracle_group_stats": (i32, [P, i32, i64, i32, i32, i64, i64, P, P]),
@@ -96,8 +96,9 @@ def philox4x32_10(ctr, key) -> np.ndarray:
     return out
 
 
-def lane16(seed: int, i: int) -> int:
-    return int(lib().oracle_lane16(seed, i))
+def rand8(seed: int, i: int) -> int:
+    """k_i in [0, 256): the random byte of element i (R3)."""
+    return int(lib().oracle_rand8(seed, i))
 
 
 def widen(x: np.ndarray, tag: int) -> np.ndarray:

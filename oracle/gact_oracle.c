@@ -21,7 +21,7 @@
  *
  * Parity status: every function here is pinned by tests/test_oracle_*.py to something
  * other than itself (KAT vectors, ATen's Philox, NumPy/torch dtype conversions, exact
- * rational arithmetic, exhaustive lane enumeration, closed-form round trips, brute force).
+ * rational arithmetic, exhaustive enumeration of the random byte, closed-form round trips, brute force).
  */
 #include "gact_oracle.h"
 
@@ -59,18 +59,21 @@ void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t
   out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
 }
 
-/* Element i draws from block i>>3 (8 elements share one Philox call, 16 bits each):
- * key = (lo32(seed), hi32(seed)), counter = (lo32(i>>3), hi32(i>>3), 0, 0), lane j = i&7
- * is the low (j even) or high (j odd) half of word j>>1. */
-uint32_t oracle_lane16(uint64_t seed, uint64_t i) {
-  uint64_t block = i >> 3;
+/* Element i draws 8 random bits (R3, R4 as revised by DESIGN.md §4's ceiling table):
+ *   block  beta(i) = 32 floor(i / 512) + (floor(i / 8) mod 32),
+ *   byte   j(i)    = 8 (floor(i / 256) mod 2) + (i mod 8)
+ * of the block's 16 output bytes (word j >> 2, byte j & 3, least significant first);
+ * key = (lo32(seed), hi32(seed)), counter = (lo32(beta), hi32(beta), 0, 0). Every block
+ * serves 16 elements: chunk l (8 consecutive elements) of the first and of the second
+ * 256-element half of each 512-element span. */
+uint32_t oracle_rand8(uint64_t seed, uint64_t i) {
+  uint64_t block = ((i >> 9) << 5) + ((i >> 3) & 31u);
   uint32_t ctr[4] = {(uint32_t)block, (uint32_t)(block >> 32), 0u, 0u};
   uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
   uint32_t r[4];
   oracle_philox4x32_10(ctr, key, r);
-  uint32_t j = (uint32_t)(i & 7u);
-  uint32_t word = r[j >> 1];
-  return (j & 1u) ? (word >> 16) : (word & 0xFFFFu);
+  uint32_t j = (uint32_t)(((i >> 8) & 1u) * 8u + (i & 7u));
+  return (r[j >> 2] >> (8u * (j & 3u))) & 0xFFu;
 }
 
 /* ------------------------------------------------------------------------------------
@@ -198,8 +201,8 @@ int32_t oracle_group_stats(const void* x, int32_t dtype, int64_t n, int32_t G, i
 /* ------------------------------------------------------------------------------------
  * R4, R5  Stochastic rounding (App. Prop. 3):
  *   Q(h)_j = T^{-1}(ceil(T(h_j)))  w.p. T(h_j) - floor(T(h_j)),  else T^{-1}(floor(T(h_j)))
- * realised as q = floor(T + u) with u = (2k+1) 2^-17, k uniform on [0, 2^16): the event
- * q = ceil(T) is {u >= 1 - frac(T)}, whose probability is frac(T) up to 2^-17 (R4).
+ * realised as q = floor(T + u) with u = (2k+1) 2^-9, k uniform on [0, 2^8): the event
+ * q = ceil(T) is {u >= 1 - frac(T)}, whose probability is frac(T) up to 2^-9 (R4).
  * T = d * inv with d = h_j - min rounded to binary32 (R5); the product and the sum with u
  * are EXACT reals (no rounding of T): q = floor(P) + [P - floor(P) >= 1 - u] with
  * P = d * inv held exactly in binary64 (24 x 24 significand bits <= 53), and
@@ -222,8 +225,8 @@ int32_t oracle_quantize_codes(const void* x, int32_t dtype, int64_t n, int32_t G
       float d = h - p.mn;                      /* h_j - min_j h   (binary32, RN) */
       double P = (double)d * (double)p.inv;    /* T = (2^b-1)(h_j - min)/(max - min), exact */
       if (!(P >= 0.0 && P <= L)) return ORACLE_EINVARIANT; /* proven in DESIGN.md R2 */
-      uint32_t k = oracle_lane16(seed, (uint64_t)i);
-      double one_minus_u = (131072.0 - 2.0 * (double)k - 1.0) / 131072.0; /* 1 - u, exact */
+      uint32_t k = oracle_rand8(seed, (uint64_t)i);
+      double one_minus_u = (512.0 - 2.0 * (double)k - 1.0) / 512.0; /* 1 - u, exact */
       double F = floor(P);
       double q = F + ((P - F) >= one_minus_u ? 1.0 : 0.0); /* floor(T + u), exact */
       if (q > L) return ORACLE_EINVARIANT;

@@ -29,8 +29,9 @@ enum { ORACLE_OK = 0, ORACLE_EINVAL = 1, ORACLE_EINFEASIBLE = 5, ORACLE_EINVARIA
 /* Philox4x32-10 block function (R3). */
 void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 
-/* The 16-bit random lane k_i of element i under `seed` (R3). */
-uint32_t oracle_lane16(uint64_t seed, uint64_t i);
+/* The 8-bit random number k_i of element i under `seed` (R3): byte 8 (i/256 mod 2) + i mod 8
+ * of Philox block 32 (i / 512) + (i / 8 mod 32). */
+uint32_t oracle_rand8(uint64_t seed, uint64_t i);
 
 /* The value of element i of a dtype-tagged buffer, widened to binary32 (exact). */
 float oracle_widen(const void* x, int32_t dtype, int64_t i);

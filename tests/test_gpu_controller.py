@@ -168,7 +168,7 @@ def _linear_closed_form(orc, h, R, bits, G=256):
     grad W = R^T h, linear in h): E||g0 - g1||^2 = 2 sum_{i,j} Var_Q[(R^T Q(h))_{ij}] with
     Var_Q[Q(h)_{bj}] = p (1 - p) scale^2 per element (independent elements, B1/B2 P:477-480),
     p = frac(T), T = (h - mn) / scale from the oracle's group statistics (p agrees with the
-    generator's exact probability to 2^-17). Returns (c, sigma of one Alg. 1 estimate): the
+    generator's exact probability to 2^-9, R4). Returns (c, sigma of one Alg. 1 estimate): the
     estimate's variance 2 sum_j tr(C_j^2) / (2 S)^2 with C_j = R^T diag(2 v_.j) R."""
     hh = h.detach().cpu().numpy().astype(np.float32)
     mn, sc = orc.group_stats(hh.reshape(-1), orc.F32, G, bits)

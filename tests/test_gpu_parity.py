@@ -324,7 +324,7 @@ def test_batch_large_groups_vs_oracle(gact, orc, dtype, G):
 
 def test_unbiased_on_gpu(gact, orc):
     """E[Q(x)] = x over 10^5 seeds of the C1 tensor: the GPU mean of
-    the decoded values is within 4.5 sigma (+ the 2^-17 lane bias) of x, and the per-element
+    the decoded values is within 4.5 sigma (+ the 2^-9 lattice bias, R4) of x, and the per-element
     variance never exceeds the paper's bound 1/4 range^2 S(b) = scale^2 / 4 (B2).
     Seeds are batched 256 per launch (one descriptor per seed, same input)."""
     G, bits, N, per = 256, 2, 100_000, 256
@@ -349,7 +349,7 @@ def test_unbiased_on_gpu(gact, orc):
     t = np.where(scale > 0, (xh.astype(np.float64) - lo) / np.maximum(scale, 1e-300), 0.0)
     p = t - np.floor(t)
     sig = np.sqrt(np.maximum(p * (1 - p), 1e-12) / N) * scale
-    tol = 4.5 * sig + (2.0 ** -17 + 1e-6) * scale + 4 * np.spacing(np.abs(xh)).astype(np.float64)
+    tol = 4.5 * sig + (2.0 ** -9 + 1e-6) * scale + 4 * np.spacing(np.abs(xh)).astype(np.float64)
     assert np.all(np.abs(mean - xh) <= tol)
     assert np.all(var <= scale ** 2 / 4 * (1 + 6 / np.sqrt(N)) + 1e-30)
 
@@ -400,7 +400,7 @@ def test_threshold_ties(gact, orc, bits, G):
     import tie_cases
     seed = 0x5EED0000 + G * 16 + bits
     ng = max(2 * 8192 // G, 2) + 3
-    xh, want = tie_cases.tie_groups(ng, G, bits, seed, orc.lane16, np.random.default_rng(G + bits))
+    xh, want = tie_cases.tie_groups(ng, G, bits, seed, orc.rand8, np.random.default_rng(G + bits))
     xh = xh[: xh.size - 5]  # ragged tail: the last group is short
     want = want[: xh.size]
     x = torch.from_numpy(xh).cuda()

@@ -75,25 +75,44 @@ def test_matches_aten_philox_engine(orc, aten_philox):
         assert [int(v) for v in orc.philox4x32_10(ctr, key)] == [int(t) for t in line.split()]
 
 
-def test_lane16_layout(orc):
-    """Element i takes 16-bit lane i&7 of block i>>3 (low half first) — checked against
-    the block function, which the two tests above pin."""
+def _bytes_of_block(orc, seed, block):
+    r = orc.philox4x32_10([block & 0xFFFFFFFF, block >> 32, 0, 0], [seed & 0xFFFFFFFF, seed >> 32])
+    return [(int(r[w]) >> (8 * b)) & 0xFF for w in range(4) for b in range(4)]  # little-endian bytes
+
+
+def test_rand8_layout(orc):
+    """Element i takes byte 8 (i/256 mod 2) + (i mod 8) of block 32 (i/512) + (i/8 mod 32)
+    (R3) -- checked against the block function, which the two tests above pin."""
     seed = 0x0123456789ABCDEF
-    for i in [0, 1, 2, 7, 8, 15, 1000, 2**33 + 5]:
-        blk = i >> 3
-        r = orc.philox4x32_10([blk & 0xFFFFFFFF, blk >> 32, 0, 0], [seed & 0xFFFFFFFF, seed >> 32])
-        j = i & 7
-        w = int(r[j >> 1])
-        expect = (w >> 16) if (j & 1) else (w & 0xFFFF)
-        assert orc.lane16(seed, i) == expect
+    for i in [0, 1, 7, 8, 255, 256, 263, 511, 512, 1000, 4095, 2**33 + 5, 2**40 + 300]:
+        blk = 32 * (i // 512) + (i // 8) % 32
+        byte = 8 * ((i // 256) % 2) + i % 8
+        assert orc.rand8(seed, i) == _bytes_of_block(orc, seed, blk)[byte], i
 
 
-def test_lanes_uniform(orc):
-    """16-bit lanes look uniform: mean of 8*4096 lanes / 2^16 within 4 sigma of 1/2, and
-    every lane position within a block has the same mean (no position bias)."""
+def test_rand8_is_a_bijection_onto_block_bytes():
+    """Over any 512-element span the (block, byte) pairs are distinct and cover 32 blocks x 16
+    bytes exactly: every random byte of the stream is used once (no two elements share one)."""
+    pairs = set()
+    base = 7 * 512
+    for i in range(base, base + 512):
+        pairs.add((32 * (i // 512) + (i // 8) % 32, 8 * ((i // 256) % 2) + i % 8))
+    assert len(pairs) == 512
+    assert {b for b, _ in pairs} == set(range(32 * 7, 32 * 8))
+    assert {j for _, j in pairs} == set(range(16))
+
+
+def test_rand8_uniform(orc):
+    """The bytes look uniform: mean of 16 x 2048 bytes / 256 within 4 sigma of the lattice
+    mean 255/512, every byte position within a block with the same mean (no position bias),
+    and all 256 values occur with frequencies within 5 sigma of 1/256."""
     seed = 99
-    k = np.array([orc.lane16(seed, i) for i in range(8 * 4096)], dtype=np.float64) / 65536.0
-    sigma = np.sqrt(1 / 12 / k.size)
-    assert abs(k.mean() - 0.5) < 4 * sigma
-    per_pos = k.reshape(-1, 8).mean(axis=0)
-    assert np.all(np.abs(per_pos - 0.5) < 4 * np.sqrt(1 / 12 / 4096))
+    k = np.array([orc.rand8(seed, i) for i in range(16 * 2048)], dtype=np.int64)
+    u = k / 256.0
+    sigma = np.sqrt((1 / 12) / u.size)
+    assert abs(u.mean() - 255 / 512) < 4 * sigma
+    pos = np.array([8 * ((i // 256) % 2) + i % 8 for i in range(k.size)])
+    for j in range(16):
+        assert abs(u[pos == j].mean() - 255 / 512) < 4 * np.sqrt((1 / 12) / (pos == j).sum())
+    f = np.bincount(k, minlength=256) / k.size
+    assert np.all(np.abs(f - 1 / 256) < 5 * np.sqrt((1 / 256) * (1 - 1 / 256) / k.size))

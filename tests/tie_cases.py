@@ -2,12 +2,12 @@
 
 Each group of G elements holds 0 and L = 2^b - 1, so mn = 0, range = L, inv = RZ(L / L) = 1
 and T_i = d_i = x_i exactly (include/gact.h). Element i of the other slots is
-x_i = N_i - (2 k_i + 1) 2^-17 + delta_i with k_i the element's 16-bit Philox lane (taken
+x_i = N_i - (2 k_i + 1) 2^-9 + delta_i with k_i the element's 8-bit Philox byte (taken
 from the oracle's generator, passed in as `lane`) and N_i in [1, L], so that
 T_i + u_i = N_i + delta_i: the threshold test floor(T + u) sits exactly on its tie for
 delta = 0 (q = N: the exact sum reaches N) and one fp32 step below / above it otherwise
 (q = N - 1 / q = N). These are the cases where a GPU shortcut for the exact real
-floor(T + u) (R5: fma.rm / fma.rn on a 2^-16 grid) would go wrong first.
+floor(T + u) (R5: fma.rm / fma.rn on the 2^-16 grid of [128, 256)) would go wrong first.
 The expected codes are the closed form above, independent of both implementations.
 """
 import numpy as np
@@ -29,7 +29,7 @@ def tie_groups(n_groups: int, G: int, bits: int, seed: int, lane, rng) -> tuple[
             k = lane(seed, i)
             N = int(rng.integers(1, L + 1))
             which = j % 3  # 0: tie, 1: just below, 2: just above
-            t = float(N) - (2 * k + 1) * 2.0 ** -17
+            t = float(N) - (2 * k + 1) * 2.0 ** -9
             # one fp32 step of t (below / above), exactly representable by construction
             f = np.float32(t)
             if float(f) != t:  # not representable at this magnitude: plain integer instead
