@@ -25,24 +25,27 @@
  * and for every element i of the group
  *     d_i = x_i - mn                                             (round to nearest)
  *     T_i = d_i * inv                                            (EXACT real product)
- *     q_i = floor(T_i + (2 k_i + 1) 2^-17),  k_i = 16-bit Philox lane of (seed, i)  (below)
+ *     q_i = floor(T_i + (2 k_i + 1) 2^-9),  k_i = random byte of (seed, i)     (below)
  *                                     (exact real floor, no rounding of T_i; q_i in [0, L]
  *                                      because T_i <= range * RZ(L / range) <= L)
  * which is T_{h,b} of P:233 followed by the stochastic rounding of P:229-230:
- * q_i = ceil(T) with probability frac(T) (up to 2^-17: u = (2k+1) 2^-17 is the centred
- * 2^-16 lattice of thresholds), else floor(T); q_i = T_i when T_i is an integer.
- * (R2, R4, R5; the GPU evaluates it exactly as fma.rm(d, inv, 64 + u) followed
- * by add.rm(., 2^23 - 64) for b = 8, and as fma.rn(d, inv, 128 + k 2^-16) -- round to
- * nearest on the 2^-16 grid of [128, 256), which adds the 2^-17 half-step -- followed by
- * add.rm(., 2^23 - 128) for b <= 4; the oracle as floor(P) + [P - floor(P) >= 1 - u] in
+ * q_i = ceil(T) with probability frac(T) rounded to the centred 2^-8 lattice of thresholds
+ * u = (2k+1) 2^-9 (|P - frac T| <= 2^-9; R4, §4a), else floor(T); q_i = T_i when
+ * T_i is an integer. (R2, R4, R5; the GPU evaluates it exactly, for every b, as
+ * add.rm(fma.rm(d, inv, 128 + u), 2^23 - 128): 128 + u is a binary32 value and rounding
+ * down never crosses an integer; the oracle as floor(P) + [P - floor(P) >= 1 - u] in
  * binary64.)
  * Decompression (T^{-1}):   y_i = fma(q_i, scale, mn) in binary32, then
  * rounded to nearest-even into the output dtype.
  *
- * Random lanes (counter-based; "seed Q^(l) with r_l" needs exact replay):
+ * Random bytes (counter-based; "seed Q^(l) with r_l" needs exact replay):
  *   Philox4x32-10 (Salmon et al. 2011, Random123 constants), key = (lo32(seed),
- *   hi32(seed)), counter = (lo32(i>>3), hi32(i>>3), 0, 0) -> words r[0..3];
- *   element i uses 16-bit lane j = i & 7: k_i = (r[j>>1] >> (16*(j&1))) & 0xFFFF.
+ *   hi32(seed)), counter = (lo32(beta), hi32(beta), 0, 0) -> words r[0..3], with
+ *     beta(i) = 32 floor(i / 512) + (floor(i / 8) mod 32),
+ *     j(i)    = 8 (floor(i / 256) mod 2) + (i mod 8),
+ *     k_i     = (r[j >> 2] >> (8 (j & 3))) & 0xFF.
+ *   Each block serves 16 elements (every byte once): the 8-element chunk at position
+ *   l = floor(i / 8) mod 32 of both 256-element halves of a 512-element span.
  *   Use a distinct seed per tensor (Alg. 1 seeds r_1..r_L); equal seeds correlate tensors.
  *
  * Packing: code q_i occupies bits [(i*b) mod 32, +b) of uint32 word (i*b)/32, LSB first;

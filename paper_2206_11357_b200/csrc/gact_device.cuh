@@ -10,7 +10,7 @@
 
 namespace gact {
 
-constexpr int kChunk = 8;       // elements per lane per Philox4x32-10 call (16-bit lanes)
+constexpr int kChunk = 8;       // elements per lane chunk (8 random bytes: half a Philox block)
 constexpr int kWarpTile = 256;  // 32 lanes x 8 elements: one coalesced warp pass
 constexpr int kWarps = 8;       // warps per CTA
 constexpr int kThreads = kWarps * 32;
@@ -157,6 +157,54 @@ __device__ __forceinline__ void philox4x32_10_xn(uint64_t blk, uint32_t k0, uint
 }
 __device__ __forceinline__ void philox4x32_10_x4(uint64_t blk, uint32_t k0, uint32_t k1, uint4 r[4]) {
   philox4x32_10_xn<4>(blk, k0, k1, r);
+}
+
+// The same shared-round form with the blocks produced one at a time (so that a kernel can
+// compute block m next to the code that consumes it): PhiloxShared holds what the N blocks
+// blk + 32 m share (round-0 word 0, the round-1 product of it, the round-1 keys, M0 c0).
+struct PhiloxShared {
+  uint64_t blk, P0;
+  uint32_t k0, k1, L, H, k0r1, k1r1;
+  bool wrap;
+};
+template <int N>
+__device__ __forceinline__ PhiloxShared philox_shared(uint64_t blk, uint32_t k0, uint32_t k1) {
+  PhiloxShared s;
+  const uint32_t c0 = (uint32_t)blk, c1 = (uint32_t)(blk >> 32);
+  s.blk = blk;
+  s.k0 = k0;
+  s.k1 = k1;
+  s.wrap = c0 > 0xFFFFFFFFu - 32u * (N - 1);
+  mul_wide(c1 ^ k0, 0xD2511F53u, s.L, s.H);
+  s.k0r1 = k0 + 0x9E3779B9u;
+  s.k1r1 = k1 + 0xBB67AE85u;
+  s.P0 = (uint64_t)c0 * 0xD2511F53u;
+  return s;
+}
+// Block blk + 32 m (bit-identical to philox4x32_10(blk + 32 m, k0, k1)).
+__device__ __forceinline__ uint4 philox_shared_block(const PhiloxShared& s, int m) {
+  if (s.wrap) return philox4x32_10(s.blk + 32u * m, s.k0, s.k1);
+  const uint64_t P = s.P0 + (uint64_t)m * (32ull * 0xD2511F53ull);
+  const uint32_t p_lo = (uint32_t)P, p_hi = (uint32_t)(P >> 32);
+  uint32_t lo1, hi1;
+  mul_wide(p_hi ^ s.k1, 0xCD9E8D57u, lo1, hi1);
+  uint32_t a0 = hi1 ^ s.k0r1, a1 = lo1, a2 = xor3(s.H, p_lo, s.k1r1), a3 = s.L;
+  uint32_t q0 = s.k0r1, q1 = s.k1r1;
+#pragma unroll
+  for (int rd = 2; rd < GACT_EXP_ROUNDS; ++rd) {
+    q0 += 0x9E3779B9u;
+    q1 += 0xBB67AE85u;
+    uint32_t l0, h0, l1, h1;
+    mul_wide(a0, 0xD2511F53u, l0, h0);
+    mul_wide(a2, 0xCD9E8D57u, l1, h1);
+    const uint32_t n0 = xor3(h1, a1, q0);
+    const uint32_t n2 = xor3(h0, a3, q1);
+    a1 = l1;
+    a3 = l0;
+    a0 = n0;
+    a2 = n2;
+  }
+  return make_uint4(a0, a1, a2, a3);
 }
 
 // ------------------------------------------------------------------- packed f32x2 math
@@ -389,15 +437,20 @@ __device__ __forceinline__ GroupParams group_params(float mn, float mx, float Lf
 
 // ----------------------------------------------------------- stochastic rounding + pack
 // Codes of 8 consecutive elements (chunk), packed LSB-first into BITS*8 bits:
-//   q_j = floor(d_j * inv + (2 k_j + 1) 2^-17),  d_j = RN(v_j - mn)     (include/gact.h)
-// with the product and the sum exact. Per pair of elements (j = 2p, 2p+1; k from the low /
-// high half of Philox word p):
-//   c = (128 + k 2^-16) + (2^-17 - 64)   PRMT builds 0x4300_0000 | k; FADD2 is exact:
-//                                         c = 64 + (2k+1) 2^-17 in [64, 65)
+//   q_j = floor(d_j * inv + (2 k_j + 1) 2^-9),  d_j = RN(v_j - mn)     (include/gact.h)
+// with the product and the sum exact; k_j is the element's random byte (R3: a chunk of 8
+// elements takes 8 consecutive bytes of its Philox block, words r.x (elements 0-3) and r.y
+// (4-7), least significant byte first). Per pair of elements (j = 2p, 2p+1), for every b:
+//   c = 128 + (2k+1) 2^-9                 one PRMT: 0x4300_0000 | k << 8 | 0x80 (exact)
 //   v = fma.rm(d, inv, c)                 FFMA2.RM: RD(d*inv + c), one rounding, downward
-//   w = add.rm(v, 2^23 - 64)              FADD2.RM: bits(w) = 0x4B00_0000 + floor(v) - 64
-// RD never crosses an integer (floor(RD(s)) = floor(s)) and [2^23, 2^24) is the integer
-// grid of binary32, so bits(w) - 0x4B00_0000 = q_j exactly. The low byte of bits(w) is q_j.
+//   w = add.rm(v, 2^23 - 128)             FADD2.RM: bits(w) = 0x4B00_0000 + floor(v) - 128
+// Every integer below 2^24 is a binary32 value, so rounding down never crosses one:
+// floor(RD(s)) = floor(s) whatever the binade of s (v < 128 + 2^b + 1 <= 385 spans
+// [128, 512) for b = 8), hence floor(v) = 128 + floor(T + u) = 128 + q; and [2^23, 2^24) is
+// the integer grid, so bits(w) - 0x4B00_0000 = q_j exactly. The low byte of bits(w) is q_j.
+// (With round 1's 16-bit lanes 128 + (2k+1) 2^-17 was not a binary32 value; the 8-bit
+// lattice point is, which saves the extra add b = 8 needed then.)
+
 template <int BITS>
 struct PackedUnit {
   uint32_t lo, hi;  // hi used only for BITS == 8 (64-bit unit)
@@ -410,44 +463,26 @@ __device__ __forceinline__ constexpr uint32_t magic_sum(int first, int count) {
   return s;
 }
 
-// w_j (= 0x4B00_0000 + q_j) of the pair (d_lo, d_hi) drawing from Philox word rw.
-// c = 64 + (2k+1) 2^-17: PRMT builds 0x4300_0000 | k = 128 + k 2^-16, then one exact FADD2
-// adds 2^-17 - 64. (Building c in the integer pipe instead -- funnel shift + lop3 -- was
-// measured slower: it overloads the ALU pipe that the Philox xors and byte permutes use.)
-//
-// b <= 4 (L <= 15) needs one instruction fewer, with bit-identical codes: with
-// c' = 128 + k 2^-16 (the PRMT result itself) every X = d*inv + c' lies in the binade
-// [128, 256), whose spacing is 2^-16, so v' = fma.rn(d, inv, c') rounds X to the nearest
-// multiple of 2^-16. v' reaches the next integer N exactly when X >= N - 2^-17 (the tie
-// X = N - 2^-17 goes to the even neighbour, N itself, as N 2^16 is even), hence
-// floor(v') = floor(X + 2^-17) = 128 + floor(T + (2k+1) 2^-17) = 128 + q. X <= 128 + L +
-// 1 - 2^-16 keeps v' below 128 + L + 1 < 256 (no binade change), and add.rm(v', 2^23 - 128)
-// gives bits 0x4B00_0000 + q as before. b = 8 (v up to 384) would cross into [256, 512),
-// spacing 2^-15, so it keeps the exact fma.rm form above.
-template <int BITS>
+// w_j (= 0x4B00_0000 + q_j) of the pair (d_lo, d_hi) whose random bytes are bytes SEL and
+// SEL + 1 of Philox word rw. (Building c in the integer pipe instead -- funnel shift + lop3
+// -- was measured slower in round 1: it overloads the ALU pipe that the Philox xors and byte
+// permutes use.)
+template <int SEL>
 __device__ __forceinline__ void code_pair(f2_t d2, f2_t inv2, uint32_t rw, uint32_t& w_lo,
                                           uint32_t& w_hi) {
-  const uint32_t klo = __byte_perm(rw, 0x43000000u, 0x7610);  // 128 + k_lo 2^-16
-  const uint32_t khi = __byte_perm(rw, 0x43000000u, 0x7632);  // 128 + k_hi 2^-16
-  f2_t w2;
-  if constexpr (BITS <= 4) {
-    const f2_t magic = f2_make(8388608.0f - 128.0f, 8388608.0f - 128.0f);
-    w2 = f2_add_rm(f2_fma_rn(d2, inv2, f2_bits(klo, khi)), magic);
-  } else {
-    const f2_t cofs = f2_make(0x1p-17f - 64.0f, 0x1p-17f - 64.0f);
-    const f2_t magic = f2_make(8388608.0f - 64.0f, 8388608.0f - 64.0f);
-    const f2_t c2 = f2_add_rn(f2_bits(klo, khi), cofs);
-    w2 = f2_add_rm(f2_fma_rm(d2, inv2, c2), magic);
-  }
-  f2_split_bits(w2, w_lo, w_hi);
+  static_assert(SEL == 0 || SEL == 2, "a pair's bytes are 0-1 or 2-3 of its word");
+  const uint32_t clo = __byte_perm(rw, 0x43000080u, 0x7604 | (SEL << 4));        // 128 + (2k+1) 2^-9
+  const uint32_t chi = __byte_perm(rw, 0x43000080u, 0x7604 | ((SEL + 1) << 4));
+  const f2_t magic = f2_make(8388608.0f - 128.0f, 8388608.0f - 128.0f);
+  f2_split_bits(f2_add_rm(f2_fma_rm(d2, inv2, f2_bits(clo, chi)), magic), w_lo, w_hi);
 }
 
 // Pack the low bytes q_j of w_j (= 0x4B00_0000 + q_j) into the chunk's 8*BITS-bit unit:
 // b = 8 by byte permutes; b < 8 by one IMAD per code (acc + (w_j << b j), mod 2^32), minus
 // the constant sum of the 0x4B00_0000 terms. Integer-pipe alternatives were measured slower
-// or equal (2^28 bf16, DESIGN.md §4): gathering the even / odd low bytes with 6 PRMT and
-// merging them (b = 1: 177 vs 166 us, b = 2: 183 vs 166, b = 4: 172 vs 167), and pairwise
-// IMAD + 3 PRMT (169 / 168 / 166): the integer pipe is as busy as the FMA-heavy pipe.
+// or equal (2^28 bf16, DESIGN.md §4, §4a): gathering the even / odd low bytes with 6 PRMT and
+// merging them, pairwise IMAD + 3 PRMT, and gathering byte 2 of the FFMA2.RN results (no
+// FADD2.RM) with byte permutes + LEA.HI: the integer pipe is as busy as the FMA-heavy pipe.
 template <int BITS>
 __device__ __forceinline__ PackedUnit<BITS> pack_codes(const uint32_t w[8]) {
   PackedUnit<BITS> out;
@@ -464,24 +499,26 @@ __device__ __forceinline__ PackedUnit<BITS> pack_codes(const uint32_t w[8]) {
   return out;
 }
 
-// Codes of the chunk's 8 elements from the 4 pairs d2[p] = (d_2p, d_2p+1), packed.
+// Codes of the chunk's 8 elements from the 4 pairs d2[p] = (d_2p, d_2p+1) and the chunk's
+// 8 random bytes r (r.x: elements 0-3, r.y: 4-7), packed.
 // (Coding each pair's odd element at scale 2^b and packing by two exact fp32 adds per pair
-// plus 3 byte permutes -- moving the packing off the FMA-heavy pipe -- was measured slower:
-// bf16 2^28, b = 1 / 2 / 4: 195 / 200 / 183 us vs 175 / 179 / 171.)
+// plus 3 byte permutes -- moving the packing off the FMA-heavy pipe -- was measured slower
+// in round 1: bf16 2^28, b = 1 / 2 / 4: 195 / 200 / 183 us vs 175 / 179 / 171.)
 template <int BITS>
-__device__ __forceinline__ PackedUnit<BITS> code_and_pack(const f2_t d2[4], float inv, uint4 r) {
-  const uint32_t words[4] = {r.x, r.y, r.z, r.w};
+__device__ __forceinline__ PackedUnit<BITS> code_and_pack(const f2_t d2[4], float inv, uint2 r) {
   const f2_t inv2 = f2_make(inv, inv);
   uint32_t w[8];
-#pragma unroll
-  for (int p = 0; p < 4; ++p) code_pair<BITS>(d2[p], inv2, words[p], w[2 * p], w[2 * p + 1]);
+  code_pair<0>(d2[0], inv2, r.x, w[0], w[1]);
+  code_pair<2>(d2[1], inv2, r.x, w[2], w[3]);
+  code_pair<0>(d2[2], inv2, r.y, w[4], w[5]);
+  code_pair<2>(d2[3], inv2, r.y, w[6], w[7]);
   return pack_codes<BITS>(w);
 }
 
 // From binary32 values (any dtype widened, or the guarded paths).
 template <int BITS>
 __device__ __forceinline__ PackedUnit<BITS> quantize_chunk(const float v[8], float mn, float inv,
-                                                           uint4 r) {
+                                                           uint2 r) {
   const f2_t mn2 = f2_make(mn, mn);
   f2_t d2[4];
 #pragma unroll
@@ -493,10 +530,10 @@ __device__ __forceinline__ PackedUnit<BITS> quantize_chunk(const float v[8], flo
 // (sub.rn.f32.bf16 / .f16: exact widening, one binary32 rounding) on each half-word.
 template <int DT, int BITS>
 __device__ __forceinline__ PackedUnit<BITS> quantize_chunk_raw(const Raw8<DT>& raw, float mn,
-                                                               float inv, uint4 r) {
+                                                               float inv, uint2 r) {
 #ifdef GACT_EXP_PHILOX_ONLY  // experiments only: cost of the random numbers alone
   PackedUnit<BITS> o;
-  o.lo = r.x ^ r.y ^ r.z ^ r.w ^ raw.a.x ^ __float_as_uint(mn + inv);
+  o.lo = r.x ^ r.y ^ raw.a.x ^ __float_as_uint(mn + inv);
   o.hi = 0;
   return o;
 #endif

@@ -17,7 +17,7 @@ struct QTensor {
   int64_t n;
   int64_t nwords;
   uint64_t seed;
-  uint64_t ctr0;  // Philox block counter of x[0]: (element offset of x in its whole tensor) / 8
+  uint64_t ctr0;  // Philox block offset of x[0]: (element offset of x in its whole tensor, a multiple of 512) / 16
 };
 
 // Launch parameters (passed by value as __grid_constant__; MAXB = 1 for single calls).

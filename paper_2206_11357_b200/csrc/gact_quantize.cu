@@ -3,7 +3,8 @@
 //
 // Work decomposition. A tensor of n elements is cut into tiles of TE = max(G, 256)
 // elements; a warp owns a tile at a time and each lane a chunk of 8 consecutive elements
-// (one Philox4x32-10 call = 8 x 16-bit lanes; one 16- or 32-byte coalesced load).
+// (8 random bytes = half a Philox4x32-10 block, R3: a lane's chunks in 256-element
+// sub-tiles 2m and 2m + 1 share one block; one 16- or 32-byte coalesced load).
 // Tensors of a batch are concatenated in tile space (QBatch::tile_start), each tensor's
 // tile count rounded up to kTileAlign = 64, so that a CTA UNIT (8 warps x U consecutive
 // tiles) never straddles two tensors. CTAs walk units grid-stride: the active window of a
@@ -12,10 +13,9 @@
 // keep it in the uniform datapath; batched launches index the descriptor table per unit).
 //  * G in {256, 512, 1024} (and 2048 for 2-byte inputs): one tile == one group, reduced in registers (FMNMX3 in-thread,
 //    one CREDUX per warp for min and max), coded from the same registers, written once:
-//    x is read exactly once. The U x CPL (8 for 2-byte inputs, 4 for fp32) Philox blocks
-//    of a lane are computed while the unit's loads are in flight (they depend only on
-//    (seed, element index)); batched launches share their rounds 0-1
-//    (philox4x32_10_xn). The U groups' divisions run on U lanes and are broadcast with
+//    x is read exactly once. The U x CPL / 2 (4 for 2-byte inputs, 2 for fp32) Philox
+//    blocks of a lane are computed while the unit's loads are in flight (they depend only
+//    on (seed, element index)), with their rounds 0-1 shared (philox4x32_10_xn). The U groups' divisions run on U lanes and are broadcast with
 //    one shuffle each.
 //  * G in {32, 64, 128}: a tile holds 256/G groups of G/8 lanes; segmented shuffles.
 //  * G = 4096 (2-byte inputs): staged in shared memory; G in {2048, 4096} fp32: the group
@@ -42,6 +42,19 @@ __device__ __forceinline__ int advance_cursor(const QBatch<MAXB>& P, int cur, in
   return cur;
 }
 
+// Random bytes (R3, include/gact.h). The chunk of 8 elements starting at element e (a multiple
+// of 8) takes half of Philox block 32 (e / 512) + (e / 8 mod 32) (+ the tensor piece's block
+// offset ctr0): words 0-1 in the first 256 elements of its 512-element span, 2-3 in the second.
+__device__ __forceinline__ uint64_t rand_block(const QTensor& T, int64_t e) {
+  return (((uint64_t)e >> 9) << 5) + (((uint64_t)e >> 3) & 31u) + T.ctr0;
+}
+__device__ __forceinline__ uint2 rand_half(uint4 r, int64_t e) {
+  return ((e >> 8) & 1) ? make_uint2(r.z, r.w) : make_uint2(r.x, r.y);
+}
+__device__ __forceinline__ uint2 chunk_rand(const QTensor& T, int64_t e) {
+  return rand_half(philox4x32_10(rand_block(T, e), (uint32_t)T.seed, (uint32_t)(T.seed >> 32)), e);
+}
+
 template <int DT>
 __device__ __forceinline__ void load8_guarded(float v[8], const void* x, int64_t e, int64_t n,
                                               float fill) {
@@ -56,8 +69,7 @@ __device__ __forceinline__ void code_chunk_guarded(const QTensor& T, int64_t e, 
                                                    float inv) {
   float v[8];
   load8_guarded<DT>(v, T.x, e, T.n, mn);
-  const uint4 r = philox4x32_10(((uint64_t)e >> 3) + T.ctr0, (uint32_t)T.seed, (uint32_t)(T.seed >> 32));
-  store_unit_guarded<BITS>(T.packed, e, T.nwords, quantize_chunk<BITS>(v, mn, inv, r));
+  store_unit_guarded<BITS>(T.packed, e, T.nwords, quantize_chunk<BITS>(v, mn, inv, chunk_rand(T, e)));
 }
 
 // One tile of a tensor with G >= 256, full or partial (the group may be short): guarded
@@ -106,15 +118,6 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 #endif
 #ifndef GACT_QS_MINB
 #define GACT_QS_MINB 3  // small-G kernel: minimum resident CTAs per SM (register cap)
-#endif
-#ifndef GACT_PHILOX_X4
-#define GACT_PHILOX_X4 1  // the 4 blocks of a lane by philox4x32_10_x4 (shared rounds 0-1)
-#endif
-#ifndef GACT_PHILOX_X4_F32
-#define GACT_PHILOX_X4_F32 1
-#endif
-#ifndef GACT_Q_RNG_EARLY
-#define GACT_Q_RNG_EARLY 64  // Philox blocks per lane computed while the unit's loads fly
 #endif
 #ifndef GACT_Q_PREFETCH
 #define GACT_Q_PREFETCH 0
@@ -189,29 +192,22 @@ __global__ void __launch_bounds__(kThreads, DT == DT_F32 ? GACT_Q_MINB_F32 : GAC
     // computed while the loads are in flight. (Computing the NEXT unit's blocks one
     // iteration ahead, or in separate producer warps fed by TMA bulk copies, were both
     // measured slower on B200: DESIGN.md §4.)
-    uint4 rnd[U][CPL];
-    const uint32_t k0 = (uint32_t)T.seed, k1 = (uint32_t)(T.seed >> 32);
-    const uint64_t blk = ((uint64_t)e_lane >> 3) + T.ctr0;
+    // The lane's chunks sit in the unit's U * CPL consecutive 256-element sub-tiles (chunk
+    // kc = k CPL + c in sub-tile kc); sub-tiles 2m and 2m + 1 take the two halves of Philox
+    // block blk0 + 32 m (R3: e_base is a multiple of 512, so blk0 = rand_block(T, e_lane)),
+    // computed with their rounds 0-1 shared (philox4x32_10_xn).
+    static_assert((U * CPL) % 2 == 0, "a unit covers whole 512-element spans");
+    uint2 rnd[U][CPL];
     if constexpr (!STATS) {
-      // Shared rounds 0-1 across the lane's blocks: with 8 blocks per lane
-      // +4-6% on batched and single-tensor launches alike.
-      if constexpr ((DT != DT_F32 || GACT_PHILOX_X4_F32) && GACT_Q_RNG_EARLY >= U * CPL &&
-                    GACT_PHILOX_X4 && !GACT_PHILOX_F64) {
-        // block offsets (k TE + c 256) / 8 = 32 (k CPL + c): the shared-round form
-        uint4 r4[U * CPL];
-        philox4x32_10_xn<U * CPL>(blk, k0, k1, r4);
+      uint4 r4[(U * CPL) / 2];
+      philox4x32_10_xn<(U * CPL) / 2>(rand_block(T, e_lane), (uint32_t)T.seed, (uint32_t)(T.seed >> 32), r4);
 #pragma unroll
-        for (int k = 0; k < U; ++k)
+      for (int k = 0; k < U; ++k)
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) rnd[k][c] = r4[k * CPL + c];
-      } else {
-#pragma unroll
-        for (int k = 0; k < U; ++k)
-#pragma unroll
-          for (int c = 0; c < CPL; ++c)
-            if (k * CPL + c < GACT_Q_RNG_EARLY)
-              rnd[k][c] = philox4x32_10(blk + (k * TE + c * kWarpTile) / kChunk, k0, k1);
-      }
+        for (int c = 0; c < CPL; ++c) {
+          const uint4 q = r4[(k * CPL + c) >> 1];
+          rnd[k][c] = ((k * CPL + c) & 1) ? make_uint2(q.z, q.w) : make_uint2(q.x, q.y);
+        }
     }
     float mnk[U], mxk[U];
 #pragma unroll
@@ -243,12 +239,9 @@ __global__ void __launch_bounds__(kThreads, DT == DT_F32 ? GACT_Q_MINB_F32 : GAC
         const float inv = __shfl_sync(kFull, gp.inv, k);
         const float mn = __fadd_rn(mnk[k], 0.0f);
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          if (k * CPL + c >= GACT_Q_RNG_EARLY)  // late blocks: computed just before use
-            rnd[k][c] = philox4x32_10(blk + (k * TE + c * kWarpTile) / kChunk, k0, k1);
+        for (int c = 0; c < CPL; ++c)
           store_unit_at<BITS>(out + ((k * TE + c * kWarpTile) * BITS) / 8,
                               quantize_chunk_raw<DT, BITS>(raw[k][c], mn, inv, rnd[k][c]));
-        }
       }
     }
   }
@@ -300,13 +293,15 @@ __global__ void __launch_bounds__(NW * 32)
     if constexpr (!STATS) {
       const uint32_t k0 = (uint32_t)T.seed, k1 = (uint32_t)(T.seed >> 32);
       for (int c = 0; c < cpl; c += 4) {
+        uint4 r;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           Raw8<DT> raw;
           lds8<DT>(raw, stage + (size_t)(c + i) * kWarpTile * ES);
           const int64_t e = e0 + (c + i) * kWarpTile + lane * kChunk;
-          const uint4 r = philox4x32_10(((uint64_t)e >> 3) + T.ctr0, k0, k1);
-          store_unit<BITS>(T.packed, e, quantize_chunk_raw<DT, BITS>(raw, gp.mn, gp.inv, r));
+          if ((i & 1) == 0) r = philox4x32_10(rand_block(T, e), k0, k1);  // sub-tiles c+i, c+i+1
+          const uint2 h = (i & 1) ? make_uint2(r.z, r.w) : make_uint2(r.x, r.y);
+          store_unit<BITS>(T.packed, e, quantize_chunk_raw<DT, BITS>(raw, gp.mn, gp.inv, h));
         }
       }
     }
@@ -348,14 +343,23 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
     for (int k = 0; k < U; ++k)
 #pragma unroll
       for (int c = 0; c < CPW; ++c) load8<DT>(raw[k][c], T.x, e_lane + k * TE + c * kWarpTile);
-    uint4 rnd[U][CPW];
+    // R3: with CPW = 2 a warp's two chunks of a group are sub-tiles 2m, 2m + 1 (one block);
+    // with CPW = 1 the pair of sub-tiles belongs to warps 2m, 2m + 1, and each computes the
+    // block and takes its half.
+    uint2 rnd[U][CPW];
     if constexpr (!STATS) {
       const uint32_t k0 = (uint32_t)T.seed, k1 = (uint32_t)(T.seed >> 32);
-      const uint64_t blk = ((uint64_t)e_lane >> 3) + T.ctr0;
 #pragma unroll
-      for (int k = 0; k < U; ++k)
-#pragma unroll
-        for (int c = 0; c < CPW; ++c) rnd[k][c] = philox4x32_10(blk + (k * TE + c * kWarpTile) / kChunk, k0, k1);
+      for (int k = 0; k < U; ++k) {
+        const int64_t e = e_lane + k * TE;
+        const uint4 r = philox4x32_10(rand_block(T, e), k0, k1);
+        if constexpr (CPW == 2) {
+          rnd[k][0] = make_uint2(r.x, r.y);
+          rnd[k][1] = make_uint2(r.z, r.w);
+        } else {
+          rnd[k][0] = rand_half(r, e);
+        }
+      }
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
@@ -410,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
 // units of 4 tiles.
 template <int DT, int BITS, bool STATS>
 __device__ __forceinline__ void small_tile(const QTensor& T, int64_t e, bool full, const Raw8<DT>& raw,
-                                           uint4 rnd, int log2g, int lpg, float Lf, int lane) {
+                                           uint2 rnd, int log2g, int lpg, float Lf, int lane) {
   float v[8];
   float lmn = FLT_MAX, lmx = -FLT_MAX;
   if (full) {
@@ -458,13 +462,18 @@ __global__ void __launch_bounds__(kThreads, GACT_QS_MINB)
     const int64_t e_lane = (cu * CU - P.tile_start[cur] + warp * U) * kWarpTile + lane * kChunk;
     const int64_t e_warp = e_lane - lane * kChunk;
     Raw8<DT> raw[U];
-    uint4 rnd[U];
+    uint2 rnd[U];
 #pragma unroll
     for (int k = 0; k < U; ++k)
       if (e_warp + (k + 1) * kWarpTile <= T.n) load8<DT>(raw[k], T.x, e_lane + k * kWarpTile);
     if constexpr (!STATS) {
-      // blocks blk + 32 k: the shared-round form (philox4x32_10_xn)
-      philox4x32_10_xn<U>(((uint64_t)e_lane >> 3) + T.ctr0, (uint32_t)T.seed, (uint32_t)(T.seed >> 32), rnd);
+      // the unit's 4 tiles are 2 whole 512-element spans (tile_start is a multiple of 64):
+      // blocks blk0, blk0 + 32 (R3), rounds 0-1 shared (philox4x32_10_xn)
+      uint4 r2[U / 2];
+      philox4x32_10_xn<U / 2>(rand_block(T, e_lane), (uint32_t)T.seed, (uint32_t)(T.seed >> 32), r2);
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        rnd[k] = (k & 1) ? make_uint2(r2[k >> 1].z, r2[k >> 1].w) : make_uint2(r2[k >> 1].x, r2[k >> 1].y);
     }
     if (e_warp + U * kWarpTile > T.n) {  // the tensor's last unit: tile by tile, guarded
 #pragma unroll
@@ -588,6 +597,22 @@ cudaError_t launch_staged_nw(const QBatch<MAXB>& p, int smem, cudaStream_t s) {
   const int grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
   kernel<<<grid, NW * 32, smem, s>>>(p);
   return cudaGetLastError();
+}
+
+// Dynamic shared memory of Kernel raised to `smem` bytes once per device (thread-safe).
+template <auto Kernel>
+cudaError_t ensure_dyn_smem(int smem) {
+  static std::atomic<int> configured[kMaxDevices];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<int>* done = dev >= 0 && dev < kMaxDevices ? &configured[dev] : nullptr;
+  if (done && smem <= done->load(std::memory_order_acquire)) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess || !done) return e;
+  int cur = done->load(std::memory_order_relaxed);
+  while (cur < smem && !done->compare_exchange_weak(cur, smem, std::memory_order_release)) {
+  }
+  return cudaSuccess;
 }
 
 // 8 warps per CTA while a warp's stage is <= 8 KB; 4 warps for 16 KB stages (fp32, G = 4096)

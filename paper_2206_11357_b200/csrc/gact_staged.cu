@@ -6,7 +6,7 @@
 // order the three ("two new streams (swap in/out) ... the CUDA event").
 //
 // A piece starting at element `off` of its tensor is quantized with the Philox block counter
-// off / 8 (QTensor::ctr0), so every result is bit-identical to the batch forms.
+// off / 16 (QTensor::ctr0), so every result is bit-identical to the batch forms.
 #include <cstring>
 #include <vector>
 
@@ -277,7 +277,7 @@ gact_status gact_quantize_pack_staged(const gact_tensor_desc* descs, int32_t cou
       it.t.n = m;
       it.t.nwords = ceil_div(m * d.bits, 32);
       it.t.seed = d.seed;
-      it.t.ctr0 = (uint64_t)off / 8;
+      it.t.ctr0 = (uint64_t)off / 16;  // R3: off is a multiple of 512, 16 elements per block
       it.dtype = d.dtype;
       it.bits = d.bits;
       return it;
