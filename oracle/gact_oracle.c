@@ -116,17 +116,43 @@ static double round_to_format(double v, int p, int emin, double vmax) {
   return r;
 }
 
+/* The same for the exact real s + e, given as an unevaluated sum with |e| <= ulp64(s) / 2
+ * (a TwoSum pair): rounded ONCE. s + e and s round alike unless s is exactly halfway
+ * between two neighbours of the format, where the sign of e breaks the tie. */
+static double round_to_format_sum(double s, double e, int p, int emin, double vmax) {
+  if (s == 0.0 || !isfinite(s)) return s + e;
+  int ex;
+  frexp(fabs(s), &ex);
+  int exp_v = ex - 1;
+  if (exp_v < emin) exp_v = emin;
+  double ulp = ldexp(1.0, exp_v - (p - 1));
+  double t = s / ulp, f = floor(t), r;
+  if (t - f == 0.5 && e != 0.0) r = (e > 0.0 ? f + 1.0 : f) * ulp;
+  else r = nearbyint(t) * ulp;
+  if (fabs(r) > vmax) return s > 0 ? INFINITY : -INFINITY;
+  return r;
+}
+
+static uint32_t encode_dtype(double r, int32_t dtype);
+
 uint32_t oracle_round_to_dtype(double v, int32_t dtype) {
-  if (dtype == ORACLE_F32) {
-    double r = round_to_format(v, 24, -126, 3.4028234663852886e38);
-    return bits_from_f32((float)r); /* r is representable: exact encoding */
-  }
-  if (dtype == ORACLE_BF16) {
-    double r = round_to_format(v, 8, -126, 3.3895313892515355e38);
-    return bits_from_f32((float)r) >> 16; /* representable in bf16: the low half is zero */
-  }
-  /* binary16: encode the representable value r from its fields */
-  double r = round_to_format(v, 11, -14, 65504.0);
+  if (dtype == ORACLE_F32) return encode_dtype(round_to_format(v, 24, -126, 3.4028234663852886e38), dtype);
+  if (dtype == ORACLE_BF16) return encode_dtype(round_to_format(v, 8, -126, 3.3895313892515355e38), dtype);
+  return encode_dtype(round_to_format(v, 11, -14, 65504.0), dtype);
+}
+
+/* s + e (a TwoSum pair) rounded once to nearest-even into dtype, encoded. */
+static uint32_t round_sum_to_dtype(double s, double e, int32_t dtype) {
+  if (dtype == ORACLE_F32) return encode_dtype(round_to_format_sum(s, e, 24, -126, 3.4028234663852886e38), dtype);
+  if (dtype == ORACLE_BF16) return encode_dtype(round_to_format_sum(s, e, 8, -126, 3.3895313892515355e38), dtype);
+  return encode_dtype(round_to_format_sum(s, e, 11, -14, 65504.0), dtype);
+}
+
+/* Encoding of a value r representable in dtype. */
+static uint32_t encode_dtype(double r, int32_t dtype) {
+  if (dtype == ORACLE_F32) return bits_from_f32((float)r);           /* exact */
+  if (dtype == ORACLE_BF16) return bits_from_f32((float)r) >> 16;    /* low half is zero */
+  /* binary16: from its fields */
   uint16_t sign = signbit(r) ? 0x8000u : 0u;
   double a = fabs(r);
   if (isinf(a)) return sign | 0x7C00u;
@@ -273,8 +299,11 @@ int32_t oracle_quantize_pack(const void* x, int32_t dtype, int64_t n, int32_t G,
 
 /* ------------------------------------------------------------------------------------
  * R7  Decompression T^{-1}_{h,b}(q) = min + q (max - min)/(2^b - 1) = mn + q * scale
- * (App. Prop. 3; "Decompressor dequantizes"). Evaluated in binary64:
- * q * scale is exact (8 x 24 bits), the sum rounds once at 2^-53.
+ * (App. Prop. 3; "Decompressor dequantizes"). oracle_dequantize_f64 gives
+ * it in binary64 (q * scale is exact, 8 x 24 bits; the sum rounds once at 2^-53);
+ * oracle_unpack_dequantize rounds the EXACT value once into the output dtype: the sum is
+ * kept as the TwoSum pair (s, e), s + e = mn + q * scale exactly (Knuth), and only then
+ * rounded (round_sum_to_dtype), so there is no double rounding through binary64.
  * ---------------------------------------------------------------------------------- */
 int32_t oracle_dequantize_f64(const uint32_t* packed, const float* mn, const float* scale,
                               int64_t n, int32_t G, int32_t bits, double* y) {
@@ -293,18 +322,22 @@ int32_t oracle_dequantize_f64(const uint32_t* packed, const float* mn, const flo
 int32_t oracle_unpack_dequantize(const uint32_t* packed, const float* mn, const float* scale,
                                  int64_t n, int32_t G, int32_t bits, void* y, int32_t y_dtype) {
   if (y_dtype < 0 || y_dtype > 2) return ORACLE_EINVAL;
-  double* v = (double*)malloc(n > 0 ? (size_t)n * sizeof(double) : 1);
-  if (!v) return ORACLE_EINVAL;
-  int32_t rc = oracle_dequantize_f64(packed, mn, scale, n, G, bits, v);
-  if (rc == ORACLE_OK) {
-    for (int64_t i = 0; i < n; ++i) {
-      uint32_t e = oracle_round_to_dtype(v[i], y_dtype);
-      if (y_dtype == ORACLE_F32) ((uint32_t*)y)[i] = e;
-      else ((uint16_t*)y)[i] = (uint16_t)e;
-    }
+  if (n < 0 || G < 1 || !(bits == 1 || bits == 2 || bits == 4 || bits == 8)) return ORACLE_EINVAL;
+  uint8_t* q = (uint8_t*)malloc(n > 0 ? (size_t)n : 1);
+  if (!q) return ORACLE_EINVAL;
+  oracle_unpack(packed, n, bits, q);
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t g = i / G;
+    double a = (double)mn[g], b = (double)q[i] * (double)scale[g]; /* both exact */
+    double s = a + b;                                               /* TwoSum (Knuth): */
+    double bv = s - a, av = s - bv;
+    double e = (a - av) + (b - bv);                                 /* s + e == a + b */
+    uint32_t enc = round_sum_to_dtype(s, e, y_dtype);
+    if (y_dtype == ORACLE_F32) ((uint32_t*)y)[i] = enc;
+    else ((uint16_t*)y)[i] = (uint16_t)enc;
   }
-  free(v);
-  return rc;
+  free(q);
+  return ORACLE_OK;
 }
 
 /* ------------------------------------------------------------------------------------
