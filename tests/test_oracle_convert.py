@@ -2,6 +2,7 @@
 library routines): widening of every bf16 and fp16 bit pattern, and round-to-nearest-even
 into fp32 / bf16 / fp16 (R7)."""
 import numpy as np
+from fractions import Fraction
 import torch
 
 
@@ -71,3 +72,38 @@ def test_round_to_bf16_matches_torch(orc):
     ref = torch.from_numpy(f).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
     got = np.array([orc.round_to_dtype(float(v), orc.BF16) for v in f], dtype=np.uint16)
     assert np.array_equal(got, ref)
+
+
+def _round_fraction_f32(F):
+    """Nearest binary32 to the exact rational F, ties to even (independent of the oracle:
+    candidates from NumPy's neighbours, chosen by exact Fraction distances)."""
+    import numpy as np
+    c = np.float32(float(F))
+    cands = {np.nextafter(c, np.float32(-np.inf)), c, np.nextafter(c, np.float32(np.inf))}
+    best = sorted(cands, key=lambda v: (abs(Fraction(float(v)) - F), int(np.array(v).view(np.uint32)) & 1))
+    return np.array(best[0], dtype=np.float32).view(np.uint32)
+
+
+def test_dequantize_rounds_the_exact_value_once(orc):
+    """R7: y = mn + q * scale rounded ONCE into the output dtype. Pins: (i) a case where
+    rounding through binary64 first is wrong -- mn = 1, q = 205, scale = 5237765 * 2^-54, so
+    q * scale = (2^30 + 1) 2^-54 = 2^-24 + 2^-54 and the exact value lies just above the
+    binary32 tie 1 + 2^-24 (binary64 would round it onto the tie, then ties-to-even to 1):
+    the answer is 1 + 2^-23; (ii) 3000 random (mn, scale, q) with large exponent gaps against
+    an exact rational rounding."""
+    import numpy as np
+    mn = np.array([1.0], dtype=np.float32)
+    sc = np.array([5237765 * 2.0 ** -54], dtype=np.float32)
+    assert float(sc[0]) == 5237765 * 2.0 ** -54
+    packed = orc.pack(np.array([205], dtype=np.uint8), 8)
+    y = orc.unpack_dequantize(packed, mn, sc, 1, 256, 8, orc.F32)
+    assert int(y[0]) == 0x3F800001
+    rng = np.random.default_rng(3)
+    n = 3000
+    mnv = (rng.standard_normal(n) * 10.0 ** rng.integers(-3, 4, n)).astype(np.float32)
+    scv = (np.abs(rng.standard_normal(n)) * np.abs(mnv) * 2.0 ** -rng.integers(8, 40, n)).astype(np.float32)
+    q = rng.integers(0, 256, n).astype(np.uint8)
+    ys = orc.unpack_dequantize(orc.pack(q, 8), mnv, scv, n, 1, 8, orc.F32)
+    for i in range(n):
+        F = Fraction(float(mnv[i])) + int(q[i]) * Fraction(float(scv[i]))
+        assert int(ys[i]) == int(_round_fraction_f32(F)), i
