@@ -164,3 +164,15 @@ def test_allocator_ties_and_errors(L, orc):
         gact.allocate_bits([float("nan")], [10], 100)
     with pytest.raises(gact.GactError):
         gact.allocate_bits([1.0], [10], 100, ladder=[2, 2])
+
+
+def test_variance_factor_matches_the_oracle(L, orc):
+    """gact_variance_factor is S(b) = (2^b - 1)^-2 of P:479-480 (S(32) = 0), equal to the
+    oracle's S and to the SPEC values S(2) = 1/9, S(4) = 1/225; -1 for invalid bits."""
+    for b in list(range(1, 17)) + [32]:
+        assert L.gact_variance_factor(b) == orc.S(b)
+    assert gact.variance_factor(2) == 1 / 9 and gact.variance_factor(4) == 1 / 225
+    for b in (0, 17, 31, 33, -1):
+        assert L.gact_variance_factor(b) == -1.0
+        with pytest.raises(ValueError):
+            gact.variance_factor(b)
