@@ -11,12 +11,15 @@
 // launch is compact in memory, each warp streams U * TE contiguous elements per step, and
 // the unit's bookkeeping (tensor, seed, pointers) is CTA-uniform (single-tensor launches
 // keep it in the uniform datapath; batched launches index the descriptor table per unit).
-//  * G in {256, 512, 1024} (and 2048 for 2-byte inputs): one tile == one group, reduced in registers (FMNMX3 in-thread,
-//    one CREDUX per warp for min and max), coded from the same registers, written once:
-//    x is read exactly once. The U x CPL / 2 (4 for 2-byte inputs, 2 for fp32) Philox
-//    blocks of a lane are computed while the unit's loads are in flight (they depend only
-//    on (seed, element index)), with their rounds 0-1 shared (philox4x32_10_xn). The U groups' divisions run on U lanes and are broadcast with
-//    one shuffle each.
+//  * G in {256, 512, 1024} (and 2048 for 2-byte inputs): one tile == one group, reduced in
+//    registers, coded from the same registers, written once: x is read exactly once. The
+//    U x CPL / 2 (4 for 2-byte inputs, 2 for fp32) Philox blocks of a lane are computed
+//    while the unit's loads are in flight (they depend only on (seed, element index)), with
+//    their rounds 0-1 shared (philox4x32_10_xn). Min / max: 2-byte inputs at G = 256 (8
+//    groups per unit) fold packed (min, -max) pairs and reduce all 8 groups with one
+//    recursive-halving butterfly (GACT_Q_XRED); otherwise FMNMX3 in-thread and one CREDUX
+//    per group for min and max. The U groups' divisions run on U lanes and are broadcast
+//    with shuffles.
 //  * G in {32, 64, 128}: a tile holds 256/G groups of G/8 lanes; segmented shuffles.
 //  * G = 4096 (2-byte inputs): staged in shared memory; G in {2048, 4096} fp32: the group
 //    spans the CTA's registers (one HBM read either way).
@@ -123,7 +126,7 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 #define GACT_Q_PREFETCH 0
 #endif
 #ifndef GACT_Q_XRED
-#define GACT_Q_XRED 0  // 2-byte, 8 groups per unit: butterfly reduction of packed (min, -max)
+#define GACT_Q_XRED 1  // 2-byte, 8 groups per unit: butterfly reduction of packed (min, -max)
 #endif
 // Chunks (Philox blocks) per lane per CTA unit: 8 for 2-byte inputs (FMA-bound: the unit's
 // 8 blocks share Philox rounds 0-1 and the key schedule / bookkeeping is amortised over 8
