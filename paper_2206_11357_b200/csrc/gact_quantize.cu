@@ -216,51 +216,51 @@ __global__ void __launch_bounds__(kThreads, DT == DT_F32 ? GACT_Q_MINB_F32 : GAC
         }
     }
 #if GACT_Q_XRED
-    if constexpr (DT != DT_F32 && U == 8 && !STATS) {
-      // 2-byte inputs, 8 groups per unit: every lane folds each tile's chunks into one packed
-      // (min, -max) pair (bf16x2 / f16x2: exact), then a recursive-halving butterfly reduces the
-      // 8 tiles across the warp at once (levels xor 16 / 8 / 4 halve the tiles a lane keeps,
-      // xor 2 / 1 finish): lane l ends with tile t(l) = 4 b4 + 2 b3 + b2 (b_i = bit i of l),
-      // computes that group's parameters, and tile k's (mn, inv) come back by two shuffles
-      // from lane 4k.
-      uint32_t p[8];
+    if constexpr (DT != DT_F32 && !STATS && U >= 2) {
+      // (U = 1, G = 2048: one CREDUX pair per unit measured 1% faster than 5 shuffle levels.)
+      // 2-byte inputs: every lane folds each of the unit's U tiles (groups) into one packed
+      // (min, -max) pair (bf16x2 / f16x2: exact), then a recursive-halving butterfly reduces
+      // the U groups across the warp at once. The first log2(U) levels (xor 16, 8, ...) halve
+      // the tiles a lane keeps (the lane with bit `mask` set keeps the upper half and sends the
+      // lower), the remaining levels finish the reduction of the one left: lane l ends with
+      // group t(l) = (l >> (5 - log2 U)) & (U - 1), computes its parameters, and group k's
+      // (mn, inv) come back by two shuffles from lane k << (5 - log2 U). For U = 8 (G = 256):
+      // 9 shuffles + 9 HMNMX2 for all 8 groups, where one CREDUX pair per group needs 16
+      // CREDUX + 16 uniform-to-vector moves + 14 selects.
+      constexpr int LU = U == 8 ? 3 : U == 4 ? 2 : U == 2 ? 1 : 0;
+      static_assert((1 << LU) == U, "U is a power of two <= 8");
+      constexpr int SH = 5 - LU;
+      uint32_t p[U];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < U; ++k) {
         p[k] = chunk_minnegmax_packed<DT>(raw[k][0]);
 #pragma unroll
         for (int c = 1; c < CPL; ++c) p[k] = min2_packed<DT>(p[k], chunk_minnegmax_packed<DT>(raw[k][c]));
       }
-      const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-      uint32_t q4[4], q2[2];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t send = b4 ? p[j] : p[j + 4], keep = b4 ? p[j + 4] : p[j];
-        q4[j] = min2_packed<DT>(keep, __shfl_xor_sync(kFull, send, 16));
+      for (int lvl = 0; lvl < LU; ++lvl) {
+        const int mask = 16 >> lvl, half = U >> (lvl + 1);
+        const bool upper = lane & mask;
+#pragma unroll
+        for (int j = 0; j < half; ++j) {
+          const uint32_t send = upper ? p[j] : p[j + half], keep = upper ? p[j + half] : p[j];
+          p[j] = min2_packed<DT>(keep, __shfl_xor_sync(kFull, send, mask));
+        }
       }
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const uint32_t send = b3 ? q4[j] : q4[j + 2], keep = b3 ? q4[j + 2] : q4[j];
-        q2[j] = min2_packed<DT>(keep, __shfl_xor_sync(kFull, send, 8));
-      }
-      uint32_t s;
-      {
-        const uint32_t send = b2 ? q2[0] : q2[1], keep = b2 ? q2[1] : q2[0];
-        s = min2_packed<DT>(keep, __shfl_xor_sync(kFull, send, 4));
-      }
-      s = min2_packed<DT>(s, __shfl_xor_sync(kFull, s, 2));
-      s = min2_packed<DT>(s, __shfl_xor_sync(kFull, s, 1));
+      for (int mask = 16 >> LU; mask >= 1; mask >>= 1) p[0] = min2_packed<DT>(p[0], __shfl_xor_sync(kFull, p[0], mask));
       float a, b;
-      unpack_minmax<DT>(s, a, b);
+      unpack_minmax<DT>(p[0], a, b);
       const GroupParams gp = group_params(a, b, Lf);
-      if ((lane & 3) == 0) {
-        const int64_t g = e_base / TE + ((lane >> 2) & 7);  // t(l)
+      if ((lane & ((1 << SH) - 1)) == 0) {
+        const int64_t g = e_base / TE + ((lane >> SH) & (U - 1));  // t(l)
         T.group_min[g] = gp.mn;
         T.group_scale[g] = gp.scale;
       }
       unsigned char* out = reinterpret_cast<unsigned char*>(T.packed) + (e_lane * BITS) / 8;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int src = 4 * k;  // a lane l with t(l) = k
+      for (int k = 0; k < U; ++k) {
+        const int src = k << SH;  // a lane l with t(l) = k
         const float inv = __shfl_sync(kFull, gp.inv, src);
         const float mn = __shfl_sync(kFull, gp.mn, src);
 #pragma unroll
