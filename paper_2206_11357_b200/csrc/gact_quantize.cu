@@ -45,6 +45,23 @@ __device__ __forceinline__ int advance_cursor(const QBatch<MAXB>& P, int cur, in
   return cur;
 }
 
+// The tensor holding tile `tile` (the last i with tile_start[i] <= tile), by binary search:
+// a CTA's first unit may lie anywhere in a launch of up to 256 tensors.
+template <int MAXB>
+__device__ __forceinline__ int first_cursor(const QBatch<MAXB>& P, int64_t tile) {
+  if constexpr (MAXB == 1) {
+    return 0;
+  } else {
+    int lo = 0, hi = P.count - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (P.tile_start[mid] <= tile) lo = mid;
+      else hi = mid - 1;
+    }
+    return lo;
+  }
+}
+
 // Random bytes (R3, include/gact.h). The chunk of 8 elements starting at element e (a multiple
 // of 8) takes half of Philox block 32 (e / 512) + (e / 8 mod 32) (+ the tensor piece's block
 // offset ctr0): words 0-1 in the first 256 elements of its 512-element span, 2-3 in the second.
@@ -165,7 +182,7 @@ __global__ void __launch_bounds__(kThreads, DT == DT_F32 ? GACT_Q_MINB_F32 : GAC
   const int warp = threadIdx.x >> 5;
   const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
   const int64_t cunits = P.tiles_total / CU;
-  int cur = 0;
+  int cur = first_cursor(P, (int64_t)blockIdx.x * CU);
   // CTA-unit bookkeeping (tensor, seed, base pointers) depends only on blockIdx and the
   // loop counter: it lives in uniform registers.
   for (int64_t cu = blockIdx.x; cu < cunits; cu += gridDim.x) {
@@ -613,6 +630,8 @@ inline int sm_count() {
 
 template <auto Kernel, typename PB>
 cudaError_t launch_persistent(const PB& p, int64_t tiles_per_warp_iter, cudaStream_t s, int waves = 1) {
+  // (One CTA per unit for launches of <= 2 / 4 x this grid -- finer balancing of the last
+  // wave of a 2^27-element tensor -- measured neutral / 3% slower: DESIGN.md §4a.)
   static const int per_sm = max_blocks_per_sm(Kernel);  // one cache per kernel
   const int64_t want = (p.tiles_total + (int64_t)kWarps * tiles_per_warp_iter - 1) /
                        ((int64_t)kWarps * tiles_per_warp_iter);
