@@ -63,7 +63,9 @@
  *    without waiting. gact_allocate_bits takes HOST pointers and runs on the host.
  *  - Validation happens before any launch; on any error nothing is written.
  *      bits not in {1,2,4,8}                          -> GACT_ERR_UNSUPPORTED_BITS
- *      group_size not a power of two in [32, 4096]    -> GACT_ERR_GROUP_SIZE
+ *      group_size not a multiple of 32 in [32, 4096]  -> GACT_ERR_GROUP_SIZE
+ *    (powers of two run specialised kernels; the other multiples of 32 a generic one: a
+ *    warp per group)
  *      x / y not 16-byte aligned, packed not 8-byte,
  *      group_min / group_scale not 4-byte aligned     -> GACT_ERR_ALIGNMENT
  *      n < 0, NULL pointer with n > 0, bad dtype      -> GACT_ERR_INVALID_ARG
@@ -171,7 +173,7 @@ gact_status gact_unpack_dequantize_batch(const gact_tensor_desc* descs, int32_t 
  * Each of data / packed / group_min / group_scale of each descriptor may be a host pointer
  * (page-locked: the copies overlap the kernels; pageable: correct, copies serialise) or a
  * device pointer; the library classifies it with cudaPointerGetAttributes. Host buffers
- * are staged through `workspace` in pieces of whole 4096-element blocks of a tensor:
+ * are staged through `workspace` in pieces of whole lcm(group_size, 4096)-element blocks:
  * GACT_STAGED_SLOTS slots of workspace_bytes / GACT_STAGED_SLOTS bytes rotate so that the
  * host->device copies of piece k+1 (internal stream), the batched kernels of piece k (on
  * `stream`) and the device->host copies of piece k-1 (second internal stream) overlap;
@@ -181,7 +183,9 @@ gact_status gact_unpack_dequantize_batch(const gact_tensor_desc* descs, int32_t 
  *                    caller-owned (contents clobbered)
  *   stream           work is ordered after everything already enqueued on `stream`
  * Same validation and alignment rules as the batch forms, plus GACT_ERR_INVALID_ARG for a
- * NULL / small / misaligned workspace. BLOCKING: returns after every output is written
+ * NULL / small / misaligned workspace. Pieces are whole multiples of lcm(group_size, 4096)
+ * elements (4096 for powers of two), so a slot must hold one such piece in the worst case
+ * (fp32, b = 8): a group size such as 4064 needs ~3 MB per slot. BLOCKING: returns after every output is written
  * (host outputs readable, device outputs complete). The internal streams and events are
  * created once per host thread and device and reused (the only state the library keeps). */
 #define GACT_STAGED_SLOTS 3

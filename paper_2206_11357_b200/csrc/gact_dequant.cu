@@ -171,16 +171,26 @@ __device__ __forceinline__ void store1(void* ybase, int64_t e, float y) {
   }
 }
 
+// The group of element e (a multiple of 8): e >> log2g for G = 2^log2g; otherwise the
+// quotient of its 8-element chunk index by G / 8 through the precomputed reciprocal
+// (DBatch::gdiv; exact for chunk indices < 2^55).
+template <bool POW2>
+__device__ __forceinline__ int64_t group_of(int64_t e, int log2g, uint64_t gdiv) {
+  if constexpr (POW2) return e >> log2g;
+  else return (int64_t)__umul64hi((uint64_t)e >> 3, gdiv);
+}
+
 // The tail of a tensor (its last, partial unit): chunk by chunk, guarded. Out of line.
 template <int DT, int BITS>
 __device__ __noinline__ void dequant_generic(const DTensor T, int64_t e_first, int chunks,
-                                             int log2g, int lane) {
+                                             int log2g, uint64_t gdiv, int lane) {
   for (int k = 0; k < chunks; ++k) {
     const int64_t e = e_first + (int64_t)k * kDequantTileElems + lane * kChunk;
     if (e >= T.n) continue;
     const uint2 unit = load_unit<BITS>(T.packed, e, T.n);
+    const int64_t g = log2g >= 0 ? group_of<true>(e, log2g, gdiv) : group_of<false>(e, log2g, gdiv);
     float y[8];
-    decode8<BITS>(unit, __ldg(T.group_min + (e >> log2g)), __ldg(T.group_scale + (e >> log2g)), y);
+    decode8<BITS>(unit, __ldg(T.group_min + g), __ldg(T.group_scale + g), y);
     if (e + kChunk <= T.n) {
       store8<DT>(T.y, e, y);
     } else {
@@ -211,7 +221,7 @@ static_assert(kDequantAlign % (kWarps * kDequantUnit) == 0, "CTA unit must divid
 // unit's tensor bookkeeping is CTA-uniform; a warp decodes U consecutive tiles of 32 x LE
 // elements (LE = 16: 256-bit stores, needs y 32-byte and packed 16-byte aligned; LE = 8:
 // 128-bit stores, the ABI's 16-byte alignment).
-template <int DT, int BITS, int MAXB, int LE>
+template <int DT, int BITS, int MAXB, int LE, bool POW2 = true>
 __global__ void __launch_bounds__(kThreads, GACT_D_MINB)
     dequantize_kernel(const __grid_constant__ DBatch<MAXB> P) {
   constexpr int U = kDequantUnit;
@@ -225,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, GACT_D_MINB)
     const DTensor& T = P.t[cur];
     const int64_t e_base = (cu * CU - P.tile_start[cur] + (int64_t)warp * U) * TE;
     if (e_base + U * TE > T.n) {
-      if (e_base < T.n) dequant_generic<DT, BITS>(T, e_base, U * TE / (int)kDequantTileElems, P.log2g, lane);
+      if (e_base < T.n) dequant_generic<DT, BITS>(T, e_base, U * TE / (int)kDequantTileElems, P.log2g, P.gdiv, lane);
       continue;
     }
     const int64_t e_lane = e_base + lane * LE;
@@ -243,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, GACT_D_MINB)
         else if constexpr (BITS == 4) unit[k][0] = make_uint2(__ldg(reinterpret_cast<const uint32_t*>(p)), 0u);
         else unit[k][0] = __ldg(reinterpret_cast<const uint2*>(p));
       }
-      const int64_t g = (e_lane + k * TE) >> P.log2g;  // LE | G: one group per lane
+      const int64_t g = group_of<POW2>(e_lane + k * TE, P.log2g, P.gdiv);  // LE | G: one group per lane
       mn[k] = __ldg(T.group_min + g);
       sc[k] = __ldg(T.group_scale + g);
     }
@@ -284,6 +294,14 @@ cudaError_t launch_dk(const PB& p, cudaStream_t s) {
 
 template <int DT, int BITS, int MAXB>
 cudaError_t launch_d(const DBatch<MAXB>& p, cudaStream_t s) {
+  if (p.log2g < 0) {  // G not a power of two: the 8-element-lane kernel with the division
+    if (p.lane_elems == 8) return launch_dk<dequantize_kernel<DT, BITS, MAXB, 8, false>>(p, s);
+    DBatch<MAXB> q = p;
+    q.lane_elems = 8;
+    for (int i = 0; i <= q.count; ++i) q.tile_start[i] *= 2;
+    q.tiles_total *= 2;
+    return launch_dk<dequantize_kernel<DT, BITS, MAXB, 8, false>>(q, s);
+  }
   if (p.lane_elems == 16 && (DT == DT_F32 || GACT_D_WIDE16)) {
     return launch_dk<dequantize_kernel<DT, BITS, MAXB, 16>>(p, s);
   }

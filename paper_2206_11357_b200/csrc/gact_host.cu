@@ -22,12 +22,8 @@ using gact::QTensor;
 bool valid_bits(int32_t b) { return b == 1 || b == 2 || b == 4 || b == 8; }
 bool valid_dtype(int32_t d) { return d == GACT_F32 || d == GACT_BF16 || d == GACT_F16; }
 
-int log2_group(int32_t G) {
-  if (G < 32 || G > 4096 || (G & (G - 1)) != 0) return -1;
-  int l = 0;
-  while ((1 << l) < G) ++l;
-  return l;
-}
+// Group sizes: multiples of 32 in [32, 4096]; powers of two take the specialised kernels.
+bool valid_group(int32_t G) { return gact::group_log2(G) >= -1; }
 
 bool aligned(const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 
@@ -92,7 +88,7 @@ namespace gact {
 
 // Items are grouped by (dtype, bits); each class is launched in chunks of <= kMaxBatch
 // items, in input order (the parameter blocks are 16 KB: kept off the stack).
-cudaError_t enqueue_quantize(const QItem* items, int32_t count, int log2g, cudaStream_t s) {
+cudaError_t enqueue_quantize(const QItem* items, int32_t count, int32_t G, cudaStream_t s) {
   static thread_local QBatch<kMaxBatch> p;
   bool seen[3][9] = {};
   for (int32_t c = 0; c < count; ++c) {
@@ -102,7 +98,8 @@ cudaError_t enqueue_quantize(const QItem* items, int32_t count, int log2g, cudaS
     int32_t i = c;
     while (i < count) {
       std::memset(&p, 0, offsetof(QBatch<kMaxBatch>, tile_start));
-      p.log2g = log2g;
+      p.log2g = group_log2(G);
+      p.group = G;
       p.Lf = (float)((1 << bits) - 1);
       int32_t m = 0;
       int64_t tiles = 0;
@@ -111,7 +108,7 @@ cudaError_t enqueue_quantize(const QItem* items, int32_t count, int log2g, cudaS
         if (it.t.n == 0 || it.dtype != dt || it.bits != bits) continue;
         p.tile_start[m] = tiles;
         p.t[m] = it.t;
-        tiles += quantize_tiles(it.t.n, log2g);
+        tiles += quantize_tiles(it.t.n, G);
         ++m;
       }
       if (m == 0) break;
@@ -125,7 +122,7 @@ cudaError_t enqueue_quantize(const QItem* items, int32_t count, int log2g, cudaS
   return cudaSuccess;
 }
 
-cudaError_t enqueue_dequantize(const DItem* items, int32_t count, int log2g, cudaStream_t s) {
+cudaError_t enqueue_dequantize(const DItem* items, int32_t count, int32_t G, cudaStream_t s) {
   static thread_local DBatch<kMaxBatch> p;
   bool seen[3][9] = {};
   for (int32_t c = 0; c < count; ++c) {
@@ -135,7 +132,8 @@ cudaError_t enqueue_dequantize(const DItem* items, int32_t count, int log2g, cud
     int32_t i = c;
     while (i < count) {
       std::memset(&p, 0, offsetof(DBatch<kMaxBatch>, tile_start));
-      p.log2g = log2g;
+      p.log2g = group_log2(G);
+      p.gdiv = p.log2g < 0 ? chunk_group_divisor(G) : 0;
       // the items this launch covers decide the lane width: wide if all are aligned for it
       int32_t m = 0;
       bool wide = true;
@@ -199,53 +197,53 @@ int64_t gact_packed_words(int64_t n, int32_t bits) {
 
 gact_status gact_group_stats(const void* x, int32_t dtype, int64_t n, int32_t group_size,
                              int32_t bits, float* group_min, float* group_scale, void* stream) {
-  const int l2 = log2_group(group_size);
   gact_status st = check_q(x, dtype, n, bits, nullptr, group_min, group_scale, false);
   if (st != GACT_OK) return st;
-  if (l2 < 0) return GACT_ERR_GROUP_SIZE;
+  if (!valid_group(group_size)) return GACT_ERR_GROUP_SIZE;
   if (n == 0) return GACT_OK;
   QBatch<1> p;
   std::memset(&p, 0, sizeof(p));
   p.count = 1;
-  p.log2g = l2;
+  p.log2g = gact::group_log2(group_size);
+  p.group = group_size;
   p.Lf = (float)((1 << bits) - 1);
   p.t[0] = make_q(x, n, bits, 0, nullptr, group_min, group_scale);
   p.tile_start[0] = 0;
-  p.tiles_total = p.tile_start[1] = gact::quantize_tiles(n, l2);
+  p.tiles_total = p.tile_start[1] = gact::quantize_tiles(n, group_size);
   return from_cuda(gact::launch_group_stats<1>(p, dtype, static_cast<cudaStream_t>(stream)));
 }
 
 gact_status gact_quantize_pack(const void* x, int32_t dtype, int64_t n, int32_t group_size,
                                int32_t bits, uint64_t seed, uint32_t* packed, float* group_min,
                                float* group_scale, void* stream) {
-  const int l2 = log2_group(group_size);
   gact_status st = check_q(x, dtype, n, bits, packed, group_min, group_scale, true);
   if (st != GACT_OK) return st;
-  if (l2 < 0) return GACT_ERR_GROUP_SIZE;
+  if (!valid_group(group_size)) return GACT_ERR_GROUP_SIZE;
   if (n == 0) return GACT_OK;
   QBatch<1> p;
   std::memset(&p, 0, sizeof(p));
   p.count = 1;
-  p.log2g = l2;
+  p.log2g = gact::group_log2(group_size);
+  p.group = group_size;
   p.Lf = (float)((1 << bits) - 1);
   p.t[0] = make_q(x, n, bits, seed, packed, group_min, group_scale);
   p.tile_start[0] = 0;
-  p.tiles_total = p.tile_start[1] = gact::quantize_tiles(n, l2);
+  p.tiles_total = p.tile_start[1] = gact::quantize_tiles(n, group_size);
   return from_cuda(gact::launch_quantize<1>(p, dtype, bits, static_cast<cudaStream_t>(stream)));
 }
 
 gact_status gact_unpack_dequantize(const uint32_t* packed, const float* group_min,
                                    const float* group_scale, int64_t n, int32_t group_size,
                                    int32_t bits, void* y, int32_t y_dtype, void* stream) {
-  const int l2 = log2_group(group_size);
   gact_status st = check_d(packed, group_min, group_scale, n, bits, y, y_dtype);
   if (st != GACT_OK) return st;
-  if (l2 < 0) return GACT_ERR_GROUP_SIZE;
+  if (!valid_group(group_size)) return GACT_ERR_GROUP_SIZE;
   if (n == 0) return GACT_OK;
   DBatch<1> p;
   std::memset(&p, 0, sizeof(p));
   p.count = 1;
-  p.log2g = l2;
+  p.log2g = gact::group_log2(group_size);
+  p.gdiv = p.log2g < 0 ? gact::chunk_group_divisor(group_size) : 0;
   p.lane_elems = wide_ok(y, packed) ? 16 : 8;
   p.t[0] = make_d(y, n, packed, group_min, group_scale);
   p.tile_start[0] = 0;
@@ -255,40 +253,38 @@ gact_status gact_unpack_dequantize(const uint32_t* packed, const float* group_mi
 
 gact_status gact_quantize_pack_batch(const gact_tensor_desc* descs, int32_t count,
                                      int32_t group_size, void* stream) {
-  const int l2 = log2_group(group_size);
   if (count < 0 || (count > 0 && !descs)) return GACT_ERR_INVALID_ARG;
   for (int32_t i = 0; i < count; ++i) {
     const gact_tensor_desc& d = descs[i];
     gact_status st = check_q(d.data, d.dtype, d.n, d.bits, d.packed, d.group_min, d.group_scale, true);
     if (st != GACT_OK) return st;
   }
-  if (l2 < 0) return GACT_ERR_GROUP_SIZE;
+  if (!valid_group(group_size)) return GACT_ERR_GROUP_SIZE;
   static thread_local std::vector<gact::QItem> items;
   items.clear();
   for (int32_t i = 0; i < count; ++i) {
     const gact_tensor_desc& d = descs[i];
     items.push_back({make_q(d.data, d.n, d.bits, d.seed, d.packed, d.group_min, d.group_scale), d.dtype, d.bits});
   }
-  return from_cuda(gact::enqueue_quantize(items.data(), count, l2, static_cast<cudaStream_t>(stream)));
+  return from_cuda(gact::enqueue_quantize(items.data(), count, group_size, static_cast<cudaStream_t>(stream)));
 }
 
 gact_status gact_unpack_dequantize_batch(const gact_tensor_desc* descs, int32_t count,
                                          int32_t group_size, void* stream) {
-  const int l2 = log2_group(group_size);
   if (count < 0 || (count > 0 && !descs)) return GACT_ERR_INVALID_ARG;
   for (int32_t i = 0; i < count; ++i) {
     const gact_tensor_desc& d = descs[i];
     gact_status st = check_d(d.packed, d.group_min, d.group_scale, d.n, d.bits, d.data, d.dtype);
     if (st != GACT_OK) return st;
   }
-  if (l2 < 0) return GACT_ERR_GROUP_SIZE;
+  if (!valid_group(group_size)) return GACT_ERR_GROUP_SIZE;
   static thread_local std::vector<gact::DItem> items;
   items.clear();
   for (int32_t i = 0; i < count; ++i) {
     const gact_tensor_desc& d = descs[i];
     items.push_back({make_d(d.data, d.n, d.packed, d.group_min, d.group_scale), d.dtype, d.bits});
   }
-  return from_cuda(gact::enqueue_dequantize(items.data(), count, l2, static_cast<cudaStream_t>(stream)));
+  return from_cuda(gact::enqueue_dequantize(items.data(), count, group_size, static_cast<cudaStream_t>(stream)));
 }
 
 // ------------------------------------------------------------------------- allocator

@@ -613,6 +613,65 @@ __global__ void __launch_bounds__(kThreads, GACT_QS_MINB)
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// G a multiple of 32 that is not a power of two (include/gact.h): one warp per group, the
+// group's G / 8 chunks strided over the lanes; min / max by CREDUX, then a second pass codes
+// the chunks (re-read: the group's <= 16 KB sit in L1 / L2). Each chunk's random bytes come
+// from its own Philox block (chunk_rand: half of the block used). Tiles = groups, 8 per CTA
+// unit (tensors padded to kTileAlign tiles). The generic path; powers of two are specialised.
+template <int DT, int BITS, int MAXB, bool STATS>
+__global__ void __launch_bounds__(kThreads)
+    quantize_anyg_kernel(const __grid_constant__ QBatch<MAXB> P) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
+  const int64_t G = P.group;
+  const int64_t cunits = P.tiles_total / kWarps;
+  int cur = first_cursor(P, (int64_t)blockIdx.x * kWarps);
+  for (int64_t cu = blockIdx.x; cu < cunits; cu += gridDim.x) {
+    cur = advance_cursor(P, cur, cu * kWarps);
+    const QTensor& T = P.t[cur];
+    const int64_t g = cu * kWarps - P.tile_start[cur] + warp;
+    const int64_t e0 = g * G;
+    if (e0 >= T.n) continue;  // alignment padding of the tile space
+    const int64_t e1 = e0 + G < T.n ? e0 + G : T.n;
+    float lmn = FLT_MAX, lmx = -FLT_MAX;  // neutral; the group has at least one element
+    for (int64_t e = e0 + lane * kChunk; e < e1; e += 32 * kChunk) {
+      if (e + kChunk <= e1) {
+        Raw8<DT> raw;
+        load8<DT>(raw, T.x, e);
+        chunk_minmax_raw<DT>(raw, lmn, lmx);
+      } else {
+        for (int j = 0; j < kChunk; ++j) {
+          if (e + j < e1) {
+            const float x = load1<DT>(T.x, e + j);
+            lmn = fminf(lmn, x);
+            lmx = fmaxf(lmx, x);
+          }
+        }
+      }
+    }
+    const GroupParams gp = group_params(warp_min(lmn), warp_max(lmx), Lf);
+    if (lane == 0) {
+      T.group_min[g] = gp.mn;
+      T.group_scale[g] = gp.scale;
+    }
+    if constexpr (!STATS) {
+      // every chunk of the group's span up to the tensor's last word: chunks past n code as
+      // zeros, which writes the zero padding of the last word (G b / 32 words per group)
+      for (int64_t e = e0 + lane * kChunk; e < e0 + G; e += 32 * kChunk) {
+        if (e + kChunk <= e1) {  // a partial chunk only ends the tensor
+          Raw8<DT> raw;
+          load8<DT>(raw, T.x, e);
+          store_unit<BITS>(T.packed, e, quantize_chunk_raw<DT, BITS>(raw, gp.mn, gp.inv, chunk_rand(T, e)));
+        } else if ((e * BITS) / 32 < T.nwords) {
+          code_chunk_guarded<DT, BITS>(T, e, gp.mn, gp.inv);
+        }
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------------- launching
 template <typename K>
 int max_blocks_per_sm(K kernel) {
@@ -707,6 +766,7 @@ cudaError_t launch_staged(const QBatch<MAXB>& p, cudaStream_t s) {
 
 template <int DT, int BITS, int MAXB, bool STATS>
 cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
+  if (p.log2g < 0) return launch_units<quantize_anyg_kernel<DT, BITS, MAXB, STATS>>(p, kWarps, s, 8);
   const int waves = DT == DT_F32 ? GACT_Q_WAVES_F32 : GACT_Q_WAVES;
   switch (p.log2g) {
     case 5:

@@ -1,6 +1,6 @@
 // gact_staged.cu — the staged (host-buffer) forms of include/gact.h: the paper's "Parallel
 // Swap and Prefetch" as one blocking call. Host buffers are cut into pieces of
-// whole 4096-element blocks and staged through GACT_STAGED_SLOTS rotating workspace slots;
+// whole lcm(G, 4096)-element blocks and staged through GACT_STAGED_SLOTS rotating workspace slots;
 // the host->device copies run on an internal swap-in stream, the batched kernels on the
 // caller's stream, the device->host copies on an internal swap-out stream, and CUDA events
 // order the three ("two new streams (swap in/out) ... the CUDA event").
@@ -16,7 +16,17 @@
 namespace {
 
 constexpr int kSlots = GACT_STAGED_SLOTS;
-constexpr int64_t kPiece = 4096;  // piece boundaries: multiples of every group size
+// Piece boundaries: multiples of 4096 (every power-of-two group size, and 512 for the Philox
+// block offset off / 16) and of G: lcm(G, 4096) elements.
+int64_t piece_elems(int32_t G) {
+  int64_t a = 4096, b = G;
+  while (b) {
+    const int64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return 4096 / a * G;
+}
 constexpr uint64_t kAlign = 256;
 
 uint64_t align_up(uint64_t v) { return (v + kAlign - 1) & ~(kAlign - 1); }
@@ -100,10 +110,10 @@ struct Copy {
 template <typename Item>
 class Pipeline {
  public:
-  Pipeline(Engine* e, char* ws, uint64_t ws_bytes, cudaStream_t s, int log2g,
-           cudaError_t (*enqueue)(const Item*, int32_t, int, cudaStream_t))
-      : e_(e), ws_(ws), slot_bytes_((ws_bytes / kSlots) & ~(kAlign - 1)), s_(s), log2g_(log2g),
-        enqueue_(enqueue) {}
+  Pipeline(Engine* e, char* ws, uint64_t ws_bytes, cudaStream_t s, int32_t G,
+           cudaError_t (*enqueue)(const Item*, int32_t, int32_t, cudaStream_t))
+      : e_(e), ws_(ws), slot_bytes_((ws_bytes / kSlots) & ~(kAlign - 1)), s_(s), G_(G),
+        piece_(piece_elems(G)), enqueue_(enqueue) {}
 
   cudaError_t begin() {
     cudaError_t r = cudaEventRecord(e_->start, s_);
@@ -135,11 +145,11 @@ class Pipeline {
     int64_t off = 0;
     while (off < n) {
       const uint64_t room = slot_bytes_ - used_;
-      // the largest piece (whole 4096-blocks, or the tensor's rest) that fits the room
-      int64_t lo = 0, hi = ceil_div(n - off, kPiece);
+      // the largest piece (whole lcm(G, 4096)-blocks, or the tensor's rest) that fits the room
+      int64_t lo = 0, hi = ceil_div(n - off, piece_);
       while (lo < hi) {
         const int64_t k = (lo + hi + 1) / 2;
-        const int64_t m = k * kPiece < n - off ? k * kPiece : n - off;
+        const int64_t m = k * piece_ < n - off ? k * piece_ : n - off;
         if (need(b, nb, s, m) <= room) lo = k; else hi = k - 1;
       }
       if (lo == 0) {
@@ -148,7 +158,7 @@ class Pipeline {
         if (r != cudaSuccess) return r;
         continue;
       }
-      const int64_t m = lo * kPiece < n - off ? lo * kPiece : n - off;
+      const int64_t m = lo * piece_ < n - off ? lo * piece_ : n - off;
       char* slot = ws_ + (uint64_t)slot_ * slot_bytes_;
       void* p[4];
       for (int i = 0; i < nb; ++i) {
@@ -178,7 +188,7 @@ class Pipeline {
       if (r == cudaSuccess) r = cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyHostToDevice, e_->in);
     if (r == cudaSuccess) r = cudaEventRecord(e_->in_done[j], e_->in);
     if (r == cudaSuccess) r = cudaStreamWaitEvent(s_, e_->in_done[j], 0);
-    if (r == cudaSuccess) r = enqueue_(items_.data(), (int32_t)items_.size(), log2g_, s_);
+    if (r == cudaSuccess) r = enqueue_(items_.data(), (int32_t)items_.size(), G_, s_);
     if (r == cudaSuccess) r = cudaEventRecord(e_->comp_done[j], s_);
     if (r == cudaSuccess) r = cudaStreamWaitEvent(e_->out, e_->comp_done[j], 0);
     for (const Copy& c : cout_)
@@ -210,8 +220,9 @@ class Pipeline {
   char* ws_;
   uint64_t slot_bytes_;
   cudaStream_t s_;
-  int log2g_;
-  cudaError_t (*enqueue_)(const Item*, int32_t, int, cudaStream_t);
+  int32_t G_;
+  int64_t piece_;
+  cudaError_t (*enqueue_)(const Item*, int32_t, int32_t, cudaStream_t);
   int slot_ = 0;
   uint64_t used_ = 0;
   bool used_slot_[kSlots] = {};
@@ -219,11 +230,11 @@ class Pipeline {
   std::vector<Copy> cin_, cout_;
 };
 
-int log2_group(int32_t G) {
-  if (G < 32 || G > 4096 || (G & (G - 1)) != 0) return -1;
-  int l = 0;
-  while ((1 << l) < G) ++l;
-  return l;
+// Bytes one whole piece needs in a slot in the worst case (fp32, b = 8, all four buffers
+// staged): the workspace must hold one per slot.
+uint64_t max_piece_bytes(int32_t G) {
+  const int64_t m = piece_elems(G);
+  return align_up((uint64_t)m * 4) + align_up((uint64_t)m) + 2 * align_up((uint64_t)(m / G) * 4);
 }
 
 // Validation shared by both directions (the batch forms' rules plus the workspace).
@@ -240,8 +251,9 @@ gact_status check_common(const gact_tensor_desc* d, int32_t count, int32_t G, co
         !aligned(t.group_scale, 4))
       return GACT_ERR_ALIGNMENT;
   }
-  if (log2_group(G) < 0) return GACT_ERR_GROUP_SIZE;
+  if (gact::group_log2(G) < -1) return GACT_ERR_GROUP_SIZE;
   if (!ws || ws_bytes < GACT_STAGED_MIN_WORKSPACE || !aligned(ws, kAlign)) return GACT_ERR_INVALID_ARG;
+  if (((ws_bytes / kSlots) & ~(kAlign - 1)) < max_piece_bytes(G)) return GACT_ERR_INVALID_ARG;
   return GACT_OK;
 }
 
@@ -256,9 +268,8 @@ gact_status gact_quantize_pack_staged(const gact_tensor_desc* descs, int32_t cou
   if (st != GACT_OK) return st;
   Engine* e = engine_for_current_device();
   if (!e) return GACT_ERR_CUDA;
-  const int l2 = log2_group(group_size);
   Pipeline<gact::QItem> pipe(e, static_cast<char*>(workspace), workspace_bytes,
-                             static_cast<cudaStream_t>(stream), l2, gact::enqueue_quantize);
+                             static_cast<cudaStream_t>(stream), group_size, gact::enqueue_quantize);
   cudaError_t r = pipe.begin();
   for (int32_t i = 0; i < count && r == cudaSuccess; ++i) {
     const gact_tensor_desc& d = descs[i];
@@ -294,9 +305,8 @@ gact_status gact_unpack_dequantize_staged(const gact_tensor_desc* descs, int32_t
   if (st != GACT_OK) return st;
   Engine* e = engine_for_current_device();
   if (!e) return GACT_ERR_CUDA;
-  const int l2 = log2_group(group_size);
   Pipeline<gact::DItem> pipe(e, static_cast<char*>(workspace), workspace_bytes,
-                             static_cast<cudaStream_t>(stream), l2, gact::enqueue_dequantize);
+                             static_cast<cudaStream_t>(stream), group_size, gact::enqueue_dequantize);
   cudaError_t r = pipe.begin();
   for (int32_t i = 0; i < count && r == cudaSuccess; ++i) {
     const gact_tensor_desc& d = descs[i];

@@ -80,7 +80,8 @@ A = 0x10000  # a 16-byte-aligned fake device address: validation never dereferen
 
 @pytest.mark.parametrize("args,expect", [
     (dict(bits=3), 2), (dict(bits=0), 2), (dict(bits=16), 2),
-    (dict(G=100), 3), (dict(G=16), 3), (dict(G=8192), 3), (dict(G=48), 3),
+    (dict(G=100), 3), (dict(G=16), 3), (dict(G=8192), 3), (dict(G=48), 3), (dict(G=4128), 3),
+    (dict(G=0), 3), (dict(G=-32), 3), (dict(G=33), 3),
     (dict(x=A + 8), 4), (dict(packed=A + 4), 4), (dict(mn=A + 2), 4),
     (dict(n=-1), 1), (dict(dtype=3), 1), (dict(x=0), 1),
 ])
@@ -93,7 +94,7 @@ def test_quantize_validation(L, args, expect):
 
 def test_dequantize_validation(L):
     assert L.gact_unpack_dequantize(A, A, A, 10, 256, 3, A, 0, None) == 2
-    assert L.gact_unpack_dequantize(A, A, A, 10, 96, 2, A, 0, None) == 3
+    assert L.gact_unpack_dequantize(A, A, A, 10, 100, 2, A, 0, None) == 3
     assert L.gact_unpack_dequantize(A, A, A, 10, 256, 2, A + 4, 0, None) == 4
     assert L.gact_unpack_dequantize(A, A, A, 10, 256, 2, A, 7, None) == 1
     assert L.gact_group_stats(A, 0, 10, 256, 5, A, A, None) == 2
@@ -132,8 +133,13 @@ def test_staged_validation_and_no_gpu(L):
         assert call(fn, ok, ws=WS + 16) == 1
         assert call(fn, ok, nbytes=MIN - 1) == 1
         assert call(fn, ok, count=-1) == 1
+        # G = 4064 (= 32 x 127) stages in pieces of lcm(4064, 4096) = 520,192 elements: the
+        # minimum workspace cannot hold one (~3 MB per slot in the worst case)
+        assert call(fn, ok, G=4064) == 1
         if not torch.cuda.is_available():
             assert call(fn, ok) == 6
+            assert call(fn, ok, G=96) == 6
+            assert call(fn, ok, G=4064, nbytes=3 * (4 << 20)) == 6
 
 
 # ---------------------------------------------------------------- host allocator parity
@@ -176,3 +182,14 @@ def test_variance_factor_matches_the_oracle(L, orc):
         assert L.gact_variance_factor(b) == -1.0
         with pytest.raises(ValueError):
             gact.variance_factor(b)
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks validation on a host without a GPU")
+@pytest.mark.parametrize("G", [32, 96, 160, 224, 256, 800, 2080, 4064, 4096])
+def test_every_multiple_of_32_is_a_valid_group_size(L, G):
+    """include/gact.h: group_size may be any multiple of 32 in [32, 4096] (powers of two take
+    the specialised kernels). Validation passes, so the call fails only at the launch
+    (GACT_ERR_CUDA, no GPU here), never with GACT_ERR_GROUP_SIZE."""
+    assert L.gact_quantize_pack(A, 1, 4096, G, 2, 1, A, A, A, None) == 6
+    assert L.gact_unpack_dequantize(A, A, A, 4096, G, 2, A, 1, None) == 6
+    assert L.gact_group_stats(A, 1, 4096, G, 2, A, A, None) == 6

@@ -188,6 +188,50 @@ def test_quantize_dequantize_parity(gact, orc, dtype, bits, G):
         check_dequantize(gact, orc, ct, ref, n, G, bits, ydt)
 
 
+GENERIC_GROUPS = [96, 160, 224, 288, 800, 1056, 2080, 4064]  # multiples of 32, not powers of two
+
+
+@pytest.mark.parametrize("dtype", DTYPES, ids=["f32", "bf16", "f16"])
+@pytest.mark.parametrize("bits", BITS)
+@pytest.mark.parametrize("G", GENERIC_GROUPS)
+def test_generic_group_sizes(gact, orc, dtype, bits, G):
+    """include/gact.h: any multiple of 32 in [32, 4096] is a group size. Those that are not
+    powers of two (generic kernels: a warp per group; the dequantize group index by an exact
+    reciprocal multiply) against the oracle: many groups, a short last group, a partial chunk,
+    and the edge groups (subnormals, signed zeros, near-overflow)."""
+    n = 37 * G + 3 * 8 + 5
+    for kind in ("normal", "edge2"):
+        x = make_input(n, dtype, seed=G * 13 + bits, kind=kind, group=G)
+        ct, ref = check_quantize(gact, orc, x, G, bits, seed=0xC0DE0000 + G * 8 + bits)
+        for ydt in DTYPES:
+            check_dequantize(gact, orc, ct, ref, n, G, bits, ydt)
+        mn, sc = gact.group_stats(x, bits, G)
+        assert torch.equal(mn, ct.group_min) and torch.equal(sc, ct.group_scale)
+
+
+@pytest.mark.parametrize("G", [96, 1056])
+def test_generic_group_sizes_batched(gact, orc, G):
+    """Batched launches with a generic G: 40 ragged tensors of mixed dtype and bits, each
+    against the oracle (CTAs start at arbitrary tensors: binary-searched cursors)."""
+    rng = np.random.default_rng(G)
+    xs, bits, seeds = [], [], []
+    for i in range(40):
+        n = int(rng.integers(1, 30 * G))
+        xs.append(make_input(n, DTYPES[i % 3], seed=2000 + i))
+        bits.append(BITS[(i // 3) % 4])
+        seeds.append(synth.tensor_seed(31, i))
+    batch = gact.quantize_pack_batch(xs, bits, seeds, G)
+    ys = gact.unpack_dequantize_batch(batch)
+    torch.cuda.synchronize()
+    for x, b, s, ct, y in zip(xs, bits, seeds, batch, ys):
+        ref_p, ref_mn, ref_sc = orc.quantize_pack(oracle_input(x), TAGS[x.dtype], G, b, s)
+        assert np.array_equal(host_bits(ct.packed), ref_p)
+        assert np.array_equal(host_bits(ct.group_min), ref_mn.view(np.uint32))
+        assert np.array_equal(host_bits(ct.group_scale), ref_sc.view(np.uint32))
+        ref_y = orc.unpack_dequantize(ref_p, ref_mn, ref_sc, x.numel(), G, b, TAGS[x.dtype])
+        assert ulp_distance(host_bits(y), ref_y, 32 if x.dtype == torch.float32 else 16).max(initial=0) <= 1
+
+
 @pytest.mark.parametrize("dtype", DTYPES, ids=["f32", "bf16", "f16"])
 @pytest.mark.parametrize("bits", BITS)
 @pytest.mark.parametrize("G", GROUPS)
@@ -508,3 +552,23 @@ def test_zz_report_dequant_mismatch_counts():
     with open(os.path.join(root, "gpurun_out", "dequant_counts.json"), "w") as f:
         json.dump(DEQUANT_COUNTS, f)
     print("dequantize mismatches (1 ulp) / values:", DEQUANT_COUNTS)
+
+
+@pytest.mark.parametrize("G", [32, 96, 256, 1056, 2048, 4064, 4096])
+def test_every_output_word_is_written(gact, orc, G):
+    """Output buffers pre-filled with ones: after one call every packed word (including the
+    zero padding of the last one) and every group statistic equals the oracle's, for every
+    kernel family and a ragged n (no word may be left unwritten)."""
+    for dtype in DTYPES:
+        for bits in BITS:
+            n = 3 * max(G, 256) + 8 * 7 + 3
+            x = make_input(n, dtype, seed=G + bits)
+            packed = torch.full((gact.packed_words(n, bits),), -1, dtype=torch.int32, device="cuda")
+            mn = torch.full((gact.num_groups(n, G),), float("nan"), device="cuda")
+            sc = torch.full_like(mn, float("nan"))
+            gact.quantize_pack(x, bits, 77, G, out=(packed, mn, sc))
+            torch.cuda.synchronize()
+            ref_p, ref_mn, ref_sc = orc.quantize_pack(oracle_input(x), TAGS[dtype], G, bits, 77)
+            assert np.array_equal(host_bits(packed), ref_p), (dtype, bits)
+            assert np.array_equal(host_bits(mn), ref_mn.view(np.uint32))
+            assert np.array_equal(host_bits(sc), ref_sc.view(np.uint32))

@@ -137,3 +137,24 @@ def test_staged_validation(gact):
     assert L.gact_quantize_pack_staged(arr, 1, 256, ws.data_ptr(), ws.numel(), s) == 0
     assert L.gact_quantize_pack_staged(ctypes.cast(None, ctypes.POINTER(gact._Desc)), 0, 256,
                                        ws.data_ptr(), ws.numel(), s) == 0
+
+
+@pytest.mark.parametrize("G", [96, 1056, 4064])
+@pytest.mark.parametrize("ws_bytes", [3 * (4 << 20), 3 * (64 << 20)])
+def test_staged_generic_group_sizes(gact, orc, G, ws_bytes):
+    """Group sizes that are not powers of two stage in pieces of lcm(G, 4096) elements (a
+    piece never splits a group, and its Philox block offset stays off / 16): bit-identical to
+    the batch forms, and the codes equal the oracle's."""
+    xs, bits, seeds = _inputs(seed=G)
+    ref = gact.quantize_pack_batch(xs, bits, seeds, G)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    got = gact.quantize_pack_staged([x.cpu().pin_memory() for x in xs], bits, seeds, G, workspace=ws)
+    ys = gact.unpack_dequantize_staged(got, workspace=ws)
+    ys_ref = gact.unpack_dequantize_batch(ref)
+    torch.cuda.synchronize()
+    for x, b, s, a, r, y, yr in zip(xs, bits, seeds, got, ref, ys, ys_ref):
+        _same(a, r)
+        assert torch.equal(y.view(-1).view(torch.uint8), yr.view(-1).view(torch.uint8))
+        p, mn, sc = orc.quantize_pack(oracle_input(x), TAGS[x.dtype], G, b, s)
+        assert np.array_equal(host_bits(a.packed), p)
+        assert np.array_equal(host_bits(a.group_min), mn.view(np.uint32))
