@@ -33,80 +33,28 @@ __device__ __forceinline__ uint32_t xor3(uint32_t a, uint32_t b, uint32_t c) {
   return d;
 }
 
-// hi32(a * m) on the FP64 pipe: with A = 2^52 + a (bit pattern {a, 0x43300000}, no
-// conversion), fma.rm(A, m 2^-32, 2^52 - 2^20 m) = 2^52 + a m 2^-32 exactly before one
-// rounding toward -inf at unit spacing, i.e. 2^52 + floor(a m / 2^32): the result's low
-// word is hi32(a m) and its high word is 0x43300000 again, so the next round's operand
-// {xor, that high word} needs no move. B200 runs DFMA at 64 lanes/clk/SM on its own pipe,
-// which takes the upper half of each 32x32->64 product off the FMA-heavy pipe (the low
-// half stays one IMAD).
-template <uint32_t M>
-__device__ __forceinline__ void mul_hi_f64(uint32_t a, uint32_t h, uint32_t& hi, uint32_t& h_out) {
-  constexpr double kScale = (double)M * (1.0 / 4294967296.0);
-  constexpr double kBias = 4503599627370496.0 - (double)M * 1048576.0;
-  asm("{\n\t.reg .f64 A, R;\n\tmov.b64 A, {%2, %3};\n\tfma.rm.f64 R, A, %4, %5;\n\t"
-      "mov.b64 {%0, %1}, R;\n\t}"
-      : "=r"(hi), "=r"(h_out)
-      : "r"(a), "r"(h), "d"(kScale), "d"(kBias));
-}
-
-#ifndef GACT_PHILOX_F64
-#define GACT_PHILOX_F64 0  // 1: upper product halves on the FP64 pipe (see mul_hi_f64)
-#endif
-
 #ifndef GACT_EXP_ROUNDS
-#define GACT_EXP_ROUNDS 10  // experiments only: Philox4x32-10 is the defined generator
+#define GACT_EXP_ROUNDS 10  // experiments only (DESIGN.md §4a table): Philox4x32-10 is the generator
 #endif
-template <bool F64>
-__device__ __forceinline__ uint4 philox4x32_10_t(uint64_t block, uint32_t k0, uint32_t k1) {
-  if constexpr (F64) {
-    // Round 0 has c2 = c3 = 0 (so M1 c2 = 0); later rounds carry the FP64 high words.
-    uint32_t c1 = (uint32_t)(block >> 32), c3, hi0, h0, h2;
-    const uint32_t a0 = (uint32_t)block;
-    mul_hi_f64<0xD2511F53u>(a0, 0x43300000u, hi0, h2);
-    c3 = a0 * 0xD2511F53u;
-    uint32_t c0 = c1 ^ k0, c2 = hi0 ^ k1;
-    c1 = 0u;
-    h0 = 0x43300000u;
+// (Round 1 also measured the upper product halves on the FP64 pipe -- fma.rm.f64 on
+// {a, 0x43300000}, bit-exact: fewer FMA-heavy cycles but more instructions, slower.)
+__device__ __forceinline__ uint4 philox4x32_10(uint64_t block, uint32_t k0, uint32_t k1) {
+  uint32_t c0 = (uint32_t)block, c1 = (uint32_t)(block >> 32), c2 = 0u, c3 = 0u;
+#pragma unroll
+  for (int r = 0; r < GACT_EXP_ROUNDS; ++r) {
+    uint32_t lo0, hi0, lo1, hi1;
+    mul_wide(c0, 0xD2511F53u, lo0, hi0);
+    mul_wide(c2, 0xCD9E8D57u, lo1, hi1);
+    const uint32_t n0 = xor3(hi1, c1, k0);
+    const uint32_t n2 = xor3(hi0, c3, k1);
+    c1 = lo1;
+    c3 = lo0;
+    c0 = n0;
+    c2 = n2;
     k0 += 0x9E3779B9u;
     k1 += 0xBB67AE85u;
-#pragma unroll
-    for (int r = 1; r < GACT_EXP_ROUNDS; ++r) {
-      uint32_t hi0, hi1, g0, g1;
-      mul_hi_f64<0xD2511F53u>(c0, h0, hi0, g0);
-      mul_hi_f64<0xCD9E8D57u>(c2, h2, hi1, g1);
-      const uint32_t lo0 = c0 * 0xD2511F53u, lo1 = c2 * 0xCD9E8D57u;
-      c0 = xor3(hi1, c1, k0);
-      h0 = g1;
-      c2 = xor3(hi0, c3, k1);
-      h2 = g0;
-      c1 = lo1;
-      c3 = lo0;
-      k0 += 0x9E3779B9u;
-      k1 += 0xBB67AE85u;
-    }
-    return make_uint4(c0, c1, c2, c3);
-  } else {
-    uint32_t c0 = (uint32_t)block, c1 = (uint32_t)(block >> 32), c2 = 0u, c3 = 0u;
-#pragma unroll
-    for (int r = 0; r < GACT_EXP_ROUNDS; ++r) {
-      uint32_t lo0, hi0, lo1, hi1;
-      mul_wide(c0, 0xD2511F53u, lo0, hi0);
-      mul_wide(c2, 0xCD9E8D57u, lo1, hi1);
-      const uint32_t n0 = xor3(hi1, c1, k0);
-      const uint32_t n2 = xor3(hi0, c3, k1);
-      c1 = lo1;
-      c3 = lo0;
-      c0 = n0;
-      c2 = n2;
-      k0 += 0x9E3779B9u;
-      k1 += 0xBB67AE85u;
-    }
-    return make_uint4(c0, c1, c2, c3);
   }
-}
-__device__ __forceinline__ uint4 philox4x32_10(uint64_t block, uint32_t k0, uint32_t k1) {
-  return philox4x32_10_t<GACT_PHILOX_F64 != 0>(block, k0, k1);
+  return make_uint4(c0, c1, c2, c3);
 }
 
 // Philox4x32-10 of the N blocks blk + 32 m, m = 0..N-1 (a lane's blocks in one quantize
@@ -155,58 +103,6 @@ __device__ __forceinline__ void philox4x32_10_xn(uint64_t blk, uint32_t k0, uint
     r[m] = make_uint4(a0, a1, a2, a3);
   }
 }
-__device__ __forceinline__ void philox4x32_10_x4(uint64_t blk, uint32_t k0, uint32_t k1, uint4 r[4]) {
-  philox4x32_10_xn<4>(blk, k0, k1, r);
-}
-
-// The same shared-round form with the blocks produced one at a time (so that a kernel can
-// compute block m next to the code that consumes it): PhiloxShared holds what the N blocks
-// blk + 32 m share (round-0 word 0, the round-1 product of it, the round-1 keys, M0 c0).
-struct PhiloxShared {
-  uint64_t blk, P0;
-  uint32_t k0, k1, L, H, k0r1, k1r1;
-  bool wrap;
-};
-template <int N>
-__device__ __forceinline__ PhiloxShared philox_shared(uint64_t blk, uint32_t k0, uint32_t k1) {
-  PhiloxShared s;
-  const uint32_t c0 = (uint32_t)blk, c1 = (uint32_t)(blk >> 32);
-  s.blk = blk;
-  s.k0 = k0;
-  s.k1 = k1;
-  s.wrap = c0 > 0xFFFFFFFFu - 32u * (N - 1);
-  mul_wide(c1 ^ k0, 0xD2511F53u, s.L, s.H);
-  s.k0r1 = k0 + 0x9E3779B9u;
-  s.k1r1 = k1 + 0xBB67AE85u;
-  s.P0 = (uint64_t)c0 * 0xD2511F53u;
-  return s;
-}
-// Block blk + 32 m (bit-identical to philox4x32_10(blk + 32 m, k0, k1)).
-__device__ __forceinline__ uint4 philox_shared_block(const PhiloxShared& s, int m) {
-  if (s.wrap) return philox4x32_10(s.blk + 32u * m, s.k0, s.k1);
-  const uint64_t P = s.P0 + (uint64_t)m * (32ull * 0xD2511F53ull);
-  const uint32_t p_lo = (uint32_t)P, p_hi = (uint32_t)(P >> 32);
-  uint32_t lo1, hi1;
-  mul_wide(p_hi ^ s.k1, 0xCD9E8D57u, lo1, hi1);
-  uint32_t a0 = hi1 ^ s.k0r1, a1 = lo1, a2 = xor3(s.H, p_lo, s.k1r1), a3 = s.L;
-  uint32_t q0 = s.k0r1, q1 = s.k1r1;
-#pragma unroll
-  for (int rd = 2; rd < GACT_EXP_ROUNDS; ++rd) {
-    q0 += 0x9E3779B9u;
-    q1 += 0xBB67AE85u;
-    uint32_t l0, h0, l1, h1;
-    mul_wide(a0, 0xD2511F53u, l0, h0);
-    mul_wide(a2, 0xCD9E8D57u, l1, h1);
-    const uint32_t n0 = xor3(h1, a1, q0);
-    const uint32_t n2 = xor3(h0, a3, q1);
-    a1 = l1;
-    a3 = l0;
-    a0 = n0;
-    a2 = n2;
-  }
-  return make_uint4(a0, a1, a2, a3);
-}
-
 // ------------------------------------------------------------------- packed f32x2 math
 // sm_100a executes these as FADD2 / FMUL2 / FFMA2 (two lanes of fp32 per instruction),
 // each lane correctly rounded in the stated mode — identical to two scalar IEEE ops.
@@ -231,16 +127,6 @@ __device__ __forceinline__ void f2_split_bits(f2_t v, uint32_t& lo, uint32_t& hi
 __device__ __forceinline__ f2_t f2_sub_rn(f2_t a, f2_t b) {
   f2_t r;
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ f2_t f2_mul_rn(f2_t a, f2_t b) {
-  f2_t r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ f2_t f2_add_rn(f2_t a, f2_t b) {
-  f2_t r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
 __device__ __forceinline__ f2_t f2_add_rm(f2_t a, f2_t b) {
@@ -289,43 +175,6 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                : "l"(p));
   return v;
-}
-
-// Bulk prefetch of [p, p + bytes) into L2 by the TMA unit (one instruction, no registers,
-// no completion tracking). p 16-byte aligned, bytes a multiple of 16.
-__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
-// ------------------------------------------------------------- mbarrier / bulk copy (TMA)
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(bar), "r"(parity) : "memory");
-}
-// One-dimensional bulk copy global -> shared through the TMA unit; completion is counted
-// in bytes on the mbarrier (complete_tx). src, dst 16-byte aligned, bytes a multiple of 16.
-__device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
 
 // 8 raw elements of one lane chunk: 32 bytes (f32) or 16 bytes (bf16 / f16).
@@ -531,12 +380,6 @@ __device__ __forceinline__ PackedUnit<BITS> quantize_chunk(const float v[8], flo
 template <int DT, int BITS>
 __device__ __forceinline__ PackedUnit<BITS> quantize_chunk_raw(const Raw8<DT>& raw, float mn,
                                                                float inv, uint2 r) {
-#ifdef GACT_EXP_PHILOX_ONLY  // experiments only: cost of the random numbers alone
-  PackedUnit<BITS> o;
-  o.lo = r.x ^ r.y ^ raw.a.x ^ __float_as_uint(mn + inv);
-  o.hi = 0;
-  return o;
-#endif
   if constexpr (DT == DT_F32) {
     float v[8];
     widen8<DT>(raw, v);

@@ -139,9 +139,6 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 #ifndef GACT_QS_MINB
 #define GACT_QS_MINB 3  // small-G kernel: minimum resident CTAs per SM (register cap)
 #endif
-#ifndef GACT_Q_PREFETCH
-#define GACT_Q_PREFETCH 0
-#endif
 #ifndef GACT_Q_XRED
 #define GACT_Q_XRED 1  // 2-byte, 8 groups per unit: butterfly reduction of packed (min, -max)
 #endif
@@ -194,17 +191,6 @@ __global__ void __launch_bounds__(kThreads, DT == DT_F32 ? GACT_Q_MINB_F32 : GAC
         if (e_base + k * TE < T.n) tile_generic<DT, BITS, STATS>(T, e_base + k * TE, P.log2g, Lf, lane);
       continue;
     }
-#if GACT_Q_PREFETCH
-    // The CTA's unit GACT_Q_PREFETCH iterations ahead (same tensor assumed; beyond its end
-    // nothing is prefetched) is pulled into L2 while this one is processed.
-    if (threadIdx.x == 0) {
-      const int64_t ahead = cu + (int64_t)GACT_Q_PREFETCH * gridDim.x;
-      const int64_t e_next = (ahead * CU - P.tile_start[cur]) * TE;
-      if (ahead < cunits && e_next + CU * TE <= T.n)
-        prefetch_l2_bulk(static_cast<const unsigned char*>(T.x) + e_next * (DT == DT_F32 ? 4 : 2),
-                         CU * TE * (DT == DT_F32 ? 4 : 2));
-    }
-#endif
     const int64_t e_lane = e_base + lane * kChunk;
     Raw8<DT> raw[U][CPL];
 #pragma unroll
