@@ -38,6 +38,8 @@ def test_bench_line_contract_single_gpu():
     assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["value"] > 0
     assert d["roofline"]["bound"] == "hbm" and 0 < d["roofline"]["frac"] < 1.5
     assert d["gpu_launches"] == 3 * 2  # one quantize + one dequantize launch per step
+    # the ~0.13 ms steps of this config are clocked too (1 ms polling + a sample after enqueue)
+    assert d["clocks"]["samples"] >= 1 and "unsampled" not in d["clocks"]["reasons"]
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
 
 
