@@ -165,6 +165,25 @@ class ClockSampler:
                 "samples": len(self.rows), "source": "nvml, 1 ms + one sample after enqueue, timed region only"}
 
 
+def pin_to_gpu_cpus(index: int):
+    """Bind this rank to the host cores nearest its GPU (NVML's CPU affinity of the device),
+    so that its host work and its pinned host buffers (the e2e leg) stay on the GPU's NUMA
+    node when N ranks share a node. Returns the number of cores, or None if unavailable."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {64 * w + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        cpus &= set(range(os.cpu_count() or 1))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return len(cpus)
+    except Exception:
+        pass
+    return None
+
+
 # ------------------------------------------------------------------------- our arm
 def run_ours(args):
     import torch
@@ -182,6 +201,7 @@ def run_ours(args):
     local = local % max(1, torch.cuda.device_count())  # several ranks per GPU only in gloo tests
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    numa = pin_to_gpu_cpus(local) if world > 1 else None  # NUMA-pinned ranks
     if world > 1:                                           # path with several ranks on one GPU
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
@@ -330,6 +350,7 @@ def run_ours(args):
             "bytes_per_step_per_rank": int(step_bytes),
             "l2": "inputs %.1f GB per rank > 126 MB L2: no flush needed" % (D.sum() * s_in / 1e9),
             "parallelism": f"dp{world} (per-rank compression + NCCL all-reduce of c)",
+            "rank_cpu_affinity": numa,
         },
         "phases": {"allreduce_us": round(host_t["allreduce_s"] / max(1, host_t["n"]) * 1e6, 1),
                    "allocate_us": round(host_t["alloc_s"] / max(1, host_t["n"]) * 1e6, 1),
