@@ -157,3 +157,34 @@ def test_bert_layer_staged_host_buffers(gact, orc):
     for x, ct, y, yr, b, s in zip(xs, got, ys, ys_ref, bits, seeds):
         assert torch.equal(y.view(torch.int16), yr.view(torch.int16))
         _check_sampled(orc, x, ct, y, int(b), s, rng, nsamples=3)
+
+
+@pytest.mark.parametrize("G", [256, 4064])
+def test_tensor_past_2_31_elements(gact, orc, G):
+    """One tensor of 2^31 + 3 * 2^20 + 77 bf16 elements (4.3 GB): 64-bit element, word and
+    group indices and Philox block counters past 2^31 / 2^32 elements, in the specialised and
+    the generic kernels. Groups at the start, around element 2^31 and at the ragged end are
+    compared with the oracle (codes, min, scale, decoded values)."""
+    n = (1 << 31) + 3 * (1 << 20) + 77
+    x = torch.randn(n, device="cuda", dtype=torch.bfloat16)
+    seed = 0xB16B00B5
+    ct = gact.quantize_pack(x, 4, seed, G)
+    y = ct.decompress()
+    torch.cuda.synchronize()
+    ng = (n + G - 1) // G
+    mid = (1 << 31) // G
+    groups = sorted({0, 1, mid - 1, mid, mid + 1, ng - 2, ng - 1} | set(np.random.default_rng(G).integers(0, ng, 8)))
+    for g in groups:
+        lo, hi = g * G, min(n, (g + 1) * G)
+        span = _host_span(x, lo, hi)
+        q, mn, sc = orc.quantize_codes_span(span, TAGS[x.dtype], n, G, 4, seed, g, g + 1)
+        assert _bits_u32(ct.group_min[g:g + 1])[0] == mn.view(np.uint32)[0], g
+        assert _bits_u32(ct.group_scale[g:g + 1])[0] == sc.view(np.uint32)[0], g
+        w0, w1 = lo * 4 // 32, (hi * 4 + 31) // 32
+        words = _bits_u32(ct.packed[w0:w1])
+        assert np.array_equal(orc.unpack(words, hi - lo, 4), q), g
+        ref = orc.unpack_dequantize(words, mn, sc, hi - lo, G, 4, TAGS[y.dtype])
+        yb = y.reshape(-1)[lo:hi].contiguous().cpu().view(torch.int16).numpy().astype(np.int64) & 0xFFFF
+        assert _ulp_distance(yb, ref.astype(np.int64), 16).max() <= 1
+    del x, y, ct
+    torch.cuda.empty_cache()
