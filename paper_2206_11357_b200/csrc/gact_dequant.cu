@@ -294,13 +294,9 @@ cudaError_t launch_dk(const PB& p, cudaStream_t s) {
 
 template <int DT, int BITS, int MAXB>
 cudaError_t launch_d(const DBatch<MAXB>& p, cudaStream_t s) {
-  if (p.log2g < 0) {  // G not a power of two: the 8-element-lane kernel with the division
-    if (p.lane_elems == 8) return launch_dk<dequantize_kernel<DT, BITS, MAXB, 8, false>>(p, s);
-    DBatch<MAXB> q = p;
-    q.lane_elems = 8;
-    for (int i = 0; i <= q.count; ++i) q.tile_start[i] *= 2;
-    q.tiles_total *= 2;
-    return launch_dk<dequantize_kernel<DT, BITS, MAXB, 8, false>>(q, s);
+  if (p.log2g < 0) {  // G not a power of two (16 | G): the same kernels with the division
+    if (p.lane_elems == 16) return launch_dk<dequantize_kernel<DT, BITS, MAXB, 16, false>>(p, s);
+    return launch_dk<dequantize_kernel<DT, BITS, MAXB, 8, false>>(p, s);
   }
   if (p.lane_elems == 16 && (DT == DT_F32 || GACT_D_WIDE16)) {
     return launch_dk<dequantize_kernel<DT, BITS, MAXB, 16>>(p, s);

@@ -476,7 +476,12 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
 
 // ---------------------------------------------------------------------------------------
 // G in {32, 64, 128}: a 256-element tile holds 256/G groups of lpg = G/8 lanes each;
-// units of 4 tiles.
+// units of U tiles (U <= lpg: a group's U divisions run on U lanes of its segment).
+#ifndef GACT_QS_UNIT
+#define GACT_QS_UNIT 8  // 2-byte inputs, G = 64 / 128: tiles per unit (G = 32 and fp32 keep 4)
+#endif
+template <int DT, int LOG2G>
+__host__ __device__ constexpr int small_unit() { return (DT != DT_F32 && LOG2G >= 6) ? GACT_QS_UNIT : 4; }
 template <int DT, int BITS, bool STATS>
 __device__ __forceinline__ void small_tile(const QTensor& T, int64_t e, bool full, const Raw8<DT>& raw,
                                            uint2 rnd, int log2g, int lpg, float Lf, int lane) {
@@ -514,7 +519,7 @@ __device__ __forceinline__ void small_tile(const QTensor& T, int64_t e, bool ful
 template <int DT, int BITS, int MAXB, bool STATS, int LOG2G>
 __global__ void __launch_bounds__(kThreads, GACT_QS_MINB)
     quantize_small_kernel(const __grid_constant__ QBatch<MAXB> P) {
-  constexpr int U = 4;
+  constexpr int U = small_unit<DT, LOG2G>();
   const int lane = threadIdx.x & 31;
   const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
   constexpr int lpg = 1 << (LOG2G - 3);  // lanes per group
@@ -756,11 +761,11 @@ cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
   const int waves = DT == DT_F32 ? GACT_Q_WAVES_F32 : GACT_Q_WAVES;
   switch (p.log2g) {
     case 5:
-      return launch_persistent<quantize_small_kernel<DT, BITS, MAXB, STATS, 5>>(p, 4, s, waves);
+      return launch_persistent<quantize_small_kernel<DT, BITS, MAXB, STATS, 5>>(p, small_unit<DT, 5>(), s, waves);
     case 6:
-      return launch_persistent<quantize_small_kernel<DT, BITS, MAXB, STATS, 6>>(p, 4, s, waves);
+      return launch_persistent<quantize_small_kernel<DT, BITS, MAXB, STATS, 6>>(p, small_unit<DT, 6>(), s, waves);
     case 7:
-      return launch_persistent<quantize_small_kernel<DT, BITS, MAXB, STATS, 7>>(p, 4, s, waves);
+      return launch_persistent<quantize_small_kernel<DT, BITS, MAXB, STATS, 7>>(p, small_unit<DT, 7>(), s, waves);
     case 8:
       return launch_persistent<quantize_big_kernel<DT, BITS, 1, MAXB, STATS>>(p, unit_tiles<DT, 1>(), s, waves);
     case 9:
