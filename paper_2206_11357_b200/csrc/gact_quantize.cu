@@ -357,6 +357,19 @@ __global__ void __launch_bounds__(NW * 32)
     }
     if constexpr (!STATS) {
       const uint32_t k0 = (uint32_t)T.seed, k1 = (uint32_t)(T.seed >> 32);
+      if (cpl == 16) {  // G = 4096: the lane's 8 blocks blk0 + 32 m, rounds 0-1 shared
+        uint4 r8[8];
+        philox4x32_10_xn<8>(rand_block(T, e0 + lane * kChunk), k0, k1, r8);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          Raw8<DT> raw;
+          lds8<DT>(raw, stage + (size_t)c * kWarpTile * ES);
+          const int64_t e = e0 + c * kWarpTile + lane * kChunk;
+          const uint2 h = (c & 1) ? make_uint2(r8[c >> 1].z, r8[c >> 1].w) : make_uint2(r8[c >> 1].x, r8[c >> 1].y);
+          store_unit<BITS>(T.packed, e, quantize_chunk_raw<DT, BITS>(raw, gp.mn, gp.inv, h));
+        }
+        continue;
+      }
       for (int c = 0; c < cpl; c += 4) {
         uint4 r;
 #pragma unroll
