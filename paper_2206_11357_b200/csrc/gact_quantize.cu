@@ -398,6 +398,8 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
   constexpr int WE = CPW * kWarpTile;         // elements of a group per warp
   constexpr int TE = kWarps * WE;             // == G
   __shared__ float red[2][U][2][kWarps];      // [parity][group][min, max][warp]
+  // CPW = 1: the random half a warp's partner computed for it ([parity][group][warp][lane])
+  __shared__ uint2 xr[2][CPW == 1 ? U : 1][kWarps][32];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
@@ -422,20 +424,24 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
 #pragma unroll
       for (int c = 0; c < CPW; ++c) load8<DT>(raw[k][c], T.x, e_lane + k * TE + c * kWarpTile);
     // R3: with CPW = 2 a warp's two chunks of a group are sub-tiles 2m, 2m + 1 (one block);
-    // with CPW = 1 the pair of sub-tiles belongs to warps 2m, 2m + 1, and each computes the
-    // block and takes its half.
+    // with CPW = 1 the pair of sub-tiles belongs to warps 2m, 2m + 1: the even warp computes
+    // the blocks of groups 0-1, the odd one those of groups 2-3, and each hands its partner
+    // the other half through shared memory (read after the unit's barrier).
     uint2 rnd[U][CPW];
+    const bool odd = warp & 1;
     if constexpr (!STATS) {
       const uint32_t k0 = (uint32_t)T.seed, k1 = (uint32_t)(T.seed >> 32);
 #pragma unroll
       for (int k = 0; k < U; ++k) {
         const int64_t e = e_lane + k * TE;
-        const uint4 r = philox4x32_10(rand_block(T, e), k0, k1);
         if constexpr (CPW == 2) {
+          const uint4 r = philox4x32_10(rand_block(T, e), k0, k1);
           rnd[k][0] = make_uint2(r.x, r.y);
           rnd[k][1] = make_uint2(r.z, r.w);
-        } else {
-          rnd[k][0] = rand_half(r, e);
+        } else if ((k >= U / 2) == odd) {
+          const uint4 r = philox4x32_10(rand_block(T, e), k0, k1);
+          rnd[k][0] = odd ? make_uint2(r.z, r.w) : make_uint2(r.x, r.y);
+          xr[par][k][warp ^ 1][lane] = odd ? make_uint2(r.x, r.y) : make_uint2(r.z, r.w);
         }
       }
     }
@@ -457,6 +463,11 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
     for (int k = 0; k < U; ++k) {
       mnk[k] = warp_min(red[par][k][0][lane & (kWarps - 1)]);
       mxk[k] = warp_max(red[par][k][1][lane & (kWarps - 1)]);
+    }
+    if constexpr (!STATS && CPW == 1) {
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if ((k >= U / 2) != odd) rnd[k][0] = xr[par][k][warp][lane];
     }
     par ^= 1;
     const int sel = lane & (U - 1);
