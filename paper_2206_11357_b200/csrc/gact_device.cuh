@@ -191,15 +191,6 @@ struct Raw8<DT_F16> {
   uint4 a;
 };
 
-template <int DT>
-__device__ __forceinline__ void lds8(Raw8<DT>& r, const unsigned char* p) {
-  if constexpr (DT == DT_F32) {
-    r.a = *reinterpret_cast<const uint4*>(p);
-    r.b = *reinterpret_cast<const uint4*>(p + 16);
-  } else {
-    r.a = *reinterpret_cast<const uint4*>(p);
-  }
-}
 
 template <int DT>
 __device__ __forceinline__ void load8(Raw8<DT>& r, const void* base, int64_t e) {

@@ -21,10 +21,9 @@
 //    per group for min and max. The U groups' divisions run on U lanes and are broadcast
 //    with shuffles.
 //  * G in {32, 64, 128}: a tile holds 256/G groups of G/8 lanes; segmented shuffles.
-//  * G = 4096 (2-byte inputs): staged in shared memory; G in {2048, 4096} fp32: the group
-//    spans the CTA's registers (one HBM read either way).
+//  * G = 4096 (2-byte inputs): the group spans a warp pair's registers; G in {2048, 4096}
+//    fp32: the group spans the CTA's registers (one HBM read either way).
 // A tensor's last tile may be partial (n % TE != 0): it takes the guarded generic path.
-#include <atomic>
 #include <cfloat>
 
 #include "gact_device.cuh"
@@ -35,7 +34,6 @@ namespace gact {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kMaxDevices = 64;
 
 template <int MAXB>
 __device__ __forceinline__ int advance_cursor(const QBatch<MAXB>& P, int cur, int64_t tile) {
@@ -151,9 +149,6 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 #ifndef GACT_Q_UNIT_F32
 #define GACT_Q_UNIT_F32 4
 #endif
-#ifndef GACT_Q_G2048_REGS
-#define GACT_Q_G2048_REGS 1
-#endif
 #ifndef GACT_Q_MINB
 #define GACT_Q_MINB 3  // 2-byte inputs: 3 CTAs per SM (80 registers): ResNet-50 +0.7%, BERT +0.6% vs 2
 #endif
@@ -169,8 +164,14 @@ static_assert(kWarps * GACT_Q_UNIT <= kTileAlign && kTileAlign % (kWarps * GACT_
               kWarps * GACT_Q_UNIT_F32 <= kTileAlign && kTileAlign % (kWarps * GACT_Q_UNIT_F32) == 0,
               "a CTA unit must divide the tile alignment");
 
+#ifndef GACT_Q_MINB_LOWB
+#define GACT_Q_MINB_LOWB 2  // 2-byte inputs, b <= GACT_Q_LOWB: 2 CTAs per SM (b = 1: +2-3% at G <= 1024; b = 2 neutral, b = 4 -1-5%)
+#endif
+#ifndef GACT_Q_LOWB
+#define GACT_Q_LOWB 1
+#endif
 template <int DT, int BITS, int CPL, int MAXB, bool STATS>
-__global__ void __launch_bounds__(kThreads, DT == DT_F32 ? GACT_Q_MINB_F32 : GACT_Q_MINB)
+__global__ void __launch_bounds__(kThreads, DT == DT_F32 ? GACT_Q_MINB_F32 : BITS <= GACT_Q_LOWB ? GACT_Q_MINB_LOWB : GACT_Q_MINB)
     quantize_big_kernel(const __grid_constant__ QBatch<MAXB> P) {
   constexpr int U = unit_tiles<DT, CPL>();
   constexpr int TE = CPL * kWarpTile;  // == G
@@ -313,75 +314,70 @@ __global__ void __launch_bounds__(kThreads, DT == DT_F32 ? GACT_Q_MINB_F32 : GAC
 }
 
 // ---------------------------------------------------------------------------------------
-// G = 4096 (and G = 2048 with GACT_Q_G2048_REGS=0), 2-byte inputs: the group does not fit in
-// one warp's registers. Pass 1 streams it from HBM once, folding min/max and parking each lane's chunks in shared memory (G * s_in bytes per warp,
-// each lane re-reads only what it wrote: no synchronisation); pass 2 codes from shared memory.
-template <int DT, int BITS, int MAXB, bool STATS, int NW>
-__global__ void __launch_bounds__(NW * 32)
-    quantize_staged_kernel(const __grid_constant__ QBatch<MAXB> P) {
-  constexpr int ES = DT == DT_F32 ? 4 : 2;
-  extern __shared__ __align__(16) unsigned char stage_smem[];
+// G = 4096, 2-byte inputs: a group spans a warp pair (2m, 2m + 1), 2048 elements = 8 chunks per
+// lane each, all in registers (x read once, no stage). Each warp reduces its half with CREDUX;
+// the pair's two (min, max) meet in shared memory behind a 64-thread named barrier (one per
+// pair and unit; double-buffered by unit parity, so the next unit's write cannot overtake the
+// partner's read). A warp's 8 chunks are 4 whole 512-element spans: its 4 Philox blocks
+// (R3) are used in full, rounds 0-1 shared.
+#ifndef GACT_Q_PAIR_MINB
+#define GACT_Q_PAIR_MINB 2  // b <= 4 (b = 8: GACT_Q_MINB)
+#endif
+template <int DT, int BITS, int MAXB, bool STATS>
+__global__ void __launch_bounds__(kThreads, BITS >= 8 ? GACT_Q_MINB : GACT_Q_PAIR_MINB)
+    quantize_pair_kernel(const __grid_constant__ QBatch<MAXB> P) {
+  constexpr int CPL = 8;
+  constexpr int WE = CPL * kWarpTile;  // elements of a group per warp
+  constexpr int TE = 2 * WE;           // == G
+  constexpr int U = kWarps / 2;        // groups per CTA unit
+  __shared__ float2 red[2][U][2];      // [parity][pair][warp of the pair] = (min, max)
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
+  const int pair = warp >> 1, half = warp & 1;
   const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
-  const int cpl = 1 << (P.log2g - 8);
-  const int64_t TE = (int64_t)1 << P.log2g;
-  unsigned char* stage = stage_smem + (size_t)warp * (TE * ES) + lane * kChunk * ES;
-  int cur = 0;
-  for (int64_t cu = blockIdx.x; cu < P.tiles_total / NW; cu += gridDim.x) {
-    cur = advance_cursor(P, cur, cu * NW);
+  const int64_t cunits = P.tiles_total / U;  // a quantize tile is one group here
+  int cur = first_cursor(P, (int64_t)blockIdx.x * U), par = 0;
+  for (int64_t cu = blockIdx.x; cu < cunits; cu += gridDim.x) {
+    cur = advance_cursor(P, cur, cu * U);
     const QTensor& T = P.t[cur];
-    const int64_t e0 = (cu * NW - P.tile_start[cur] + warp) * TE;
-    if (e0 >= T.n) continue;  // alignment padding of the tile space
-    if (e0 + TE > T.n) {
-      tile_generic<DT, BITS, STATS>(T, e0, P.log2g, Lf, lane);
-      continue;
+    const int64_t e_unit = (cu * U - P.tile_start[cur]) * TE;
+    if (e_unit + U * TE > T.n) {  // CTA-uniform: the tensor's last unit, warp k codes group k
+      if (warp < U && e_unit + warp * TE < T.n)
+        tile_generic<DT, BITS, STATS>(T, e_unit + warp * TE, P.log2g, Lf, lane);
+      continue;  // no barrier, `par` unchanged
+    }
+    const int64_t e_lane = e_unit + pair * TE + half * WE + lane * kChunk;
+    Raw8<DT> raw[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) load8<DT>(raw[c], T.x, e_lane + c * kWarpTile);
+    uint2 rnd[CPL];
+    if constexpr (!STATS) {
+      uint4 r4[CPL / 2];
+      philox4x32_10_xn<CPL / 2>(rand_block(T, e_lane), (uint32_t)T.seed, (uint32_t)(T.seed >> 32), r4);
+#pragma unroll
+      for (int c = 0; c < CPL; ++c)
+        rnd[c] = (c & 1) ? make_uint2(r4[c >> 1].z, r4[c >> 1].w) : make_uint2(r4[c >> 1].x, r4[c >> 1].y);
     }
     float lmn = FLT_MAX, lmx = -FLT_MAX;
-    for (int c = 0; c < cpl; c += 4) {
-      Raw8<DT> raw[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) load8<DT>(raw[i], T.x, e0 + (c + i) * kWarpTile + lane * kChunk);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        chunk_minmax_raw<DT>(raw[i], lmn, lmx);
-        unsigned char* d = stage + (size_t)(c + i) * kWarpTile * ES;
-        *reinterpret_cast<uint4*>(d) = raw[i].a;
-        if constexpr (DT == DT_F32) *reinterpret_cast<uint4*>(d + 16) = raw[i].b;
-      }
-    }
-    const GroupParams gp = group_params(warp_min(lmn), warp_max(lmx), Lf);
-    if (lane == 0) {
-      T.group_min[e0 >> P.log2g] = gp.mn;
-      T.group_scale[e0 >> P.log2g] = gp.scale;
+    for (int c = 0; c < CPL; ++c) chunk_minmax_raw<DT>(raw[c], lmn, lmx);
+    lmn = warp_min(lmn);
+    lmx = warp_max(lmx);
+    if (lane == 0) red[par][pair][half] = make_float2(lmn, lmx);
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+    const float2 o = red[par][pair][half ^ 1];
+    par ^= 1;
+    const GroupParams gp = group_params(fminf(lmn, o.x), fmaxf(lmx, o.y), Lf);
+    if (half == 0 && lane == 0) {
+      const int64_t g = (e_unit >> P.log2g) + pair;
+      T.group_min[g] = gp.mn;
+      T.group_scale[g] = gp.scale;
     }
     if constexpr (!STATS) {
-      const uint32_t k0 = (uint32_t)T.seed, k1 = (uint32_t)(T.seed >> 32);
-      if (cpl == 16) {  // G = 4096: the lane's 8 blocks blk0 + 32 m, rounds 0-1 shared
-        uint4 r8[8];
-        philox4x32_10_xn<8>(rand_block(T, e0 + lane * kChunk), k0, k1, r8);
+      unsigned char* out = reinterpret_cast<unsigned char*>(T.packed) + (e_lane * BITS) / 8;
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          Raw8<DT> raw;
-          lds8<DT>(raw, stage + (size_t)c * kWarpTile * ES);
-          const int64_t e = e0 + c * kWarpTile + lane * kChunk;
-          const uint2 h = (c & 1) ? make_uint2(r8[c >> 1].z, r8[c >> 1].w) : make_uint2(r8[c >> 1].x, r8[c >> 1].y);
-          store_unit<BITS>(T.packed, e, quantize_chunk_raw<DT, BITS>(raw, gp.mn, gp.inv, h));
-        }
-        continue;
-      }
-      for (int c = 0; c < cpl; c += 4) {
-        uint4 r;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          Raw8<DT> raw;
-          lds8<DT>(raw, stage + (size_t)(c + i) * kWarpTile * ES);
-          const int64_t e = e0 + (c + i) * kWarpTile + lane * kChunk;
-          if ((i & 1) == 0) r = philox4x32_10(rand_block(T, e), k0, k1);  // sub-tiles c+i, c+i+1
-          const uint2 h = (i & 1) ? make_uint2(r.z, r.w) : make_uint2(r.x, r.y);
-          store_unit<BITS>(T.packed, e, quantize_chunk_raw<DT, BITS>(raw, gp.mn, gp.inv, h));
-        }
-      }
+      for (int c = 0; c < CPL; ++c)
+        store_unit_at<BITS>(out + (c * kWarpTile * BITS) / 8, quantize_chunk_raw<DT, BITS>(raw[c], gp.mn, gp.inv, rnd[c]));
     }
   }
 }
@@ -726,59 +722,6 @@ cudaError_t launch_units(const PB& p, int64_t tiles_per_unit, cudaStream_t s, in
   return cudaGetLastError();
 }
 
-template <int DT, int BITS, int MAXB, bool STATS, int NW>
-cudaError_t launch_staged_nw(const QBatch<MAXB>& p, int smem, cudaStream_t s) {
-  constexpr auto kernel = quantize_staged_kernel<DT, BITS, MAXB, STATS, NW>;
-  // Largest dynamic shared-memory size enabled so far, per device (the attribute belongs to
-  // the device's context); atomic because the C ABI may be called from several host threads.
-  static std::atomic<int> configured[kMaxDevices];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::atomic<int>* done = dev >= 0 && dev < kMaxDevices ? &configured[dev] : nullptr;
-  if (!done || smem > done->load(std::memory_order_acquire)) {
-    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    if (done) {
-      int cur = done->load(std::memory_order_relaxed);
-      while (cur < smem && !done->compare_exchange_weak(cur, smem, std::memory_order_release)) {
-      }
-    }
-  }
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, NW * 32, smem) != cudaSuccess || per_sm < 1)
-    per_sm = 1;
-  const int64_t want = p.tiles_total / NW;
-  const int64_t cap = (int64_t)sm_count() * per_sm;
-  const int grid = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
-  kernel<<<grid, NW * 32, smem, s>>>(p);
-  return cudaGetLastError();
-}
-
-// Dynamic shared memory of Kernel raised to `smem` bytes once per device (thread-safe).
-template <auto Kernel>
-cudaError_t ensure_dyn_smem(int smem) {
-  static std::atomic<int> configured[kMaxDevices];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::atomic<int>* done = dev >= 0 && dev < kMaxDevices ? &configured[dev] : nullptr;
-  if (done && smem <= done->load(std::memory_order_acquire)) return cudaSuccess;
-  const cudaError_t e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess || !done) return e;
-  int cur = done->load(std::memory_order_relaxed);
-  while (cur < smem && !done->compare_exchange_weak(cur, smem, std::memory_order_release)) {
-  }
-  return cudaSuccess;
-}
-
-// 8 warps per CTA while a warp's stage is <= 8 KB; 4 warps for 16 KB stages (fp32, G = 4096)
-// so that several CTAs fit an SM.
-template <int DT, int BITS, int MAXB, bool STATS>
-cudaError_t launch_staged(const QBatch<MAXB>& p, cudaStream_t s) {
-  const int per_warp = (1 << p.log2g) * (DT == DT_F32 ? 4 : 2);
-  if (per_warp > 8192) return launch_staged_nw<DT, BITS, MAXB, STATS, 4>(p, 4 * per_warp, s);
-  return launch_staged_nw<DT, BITS, MAXB, STATS, kWarps>(p, kWarps * per_warp, s);
-}
-
 template <int DT, int BITS, int MAXB, bool STATS>
 cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
   if (p.log2g < 0) return launch_units<quantize_anyg_kernel<DT, BITS, MAXB, STATS>>(p, kWarps, s, 8);
@@ -797,19 +740,19 @@ cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
     case 10:
       return launch_persistent<quantize_big_kernel<DT, BITS, 4, MAXB, STATS>>(p, unit_tiles<DT, 4>(), s, waves);
     case 11:
-      // 2-byte inputs, G = 2048: one group per warp, 8 chunks per lane, all in registers
-      // (the 8-chunk unit of G = 256 with U = 1 tile), read once.
-      if constexpr (DT != DT_F32 && GACT_Q_G2048_REGS)
+      if constexpr (DT != DT_F32) {
+        // 2-byte inputs: one group per warp, 8 chunks per lane, all in registers (the 8-chunk
+        // unit of G = 256 with U = 1 tile), read once.
         return launch_persistent<quantize_big_kernel<DT, BITS, 8, MAXB, STATS>>(p, unit_tiles<DT, 8>(), s, waves);
-      [[fallthrough]];
-    default:
-      // fp32 (HBM-bound): the group spread over the CTA in registers (+10-24%); 2-byte inputs
-      // (FMA-bound): the per-warp shared-memory stage, which needs no CTA barrier.
-      if constexpr (DT == DT_F32) {
-        if (p.log2g == 11) return launch_units<quantize_cta_kernel<DT, BITS, 1, MAXB, STATS>>(p, 4, s, waves);
-        return launch_units<quantize_cta_kernel<DT, BITS, 2, MAXB, STATS>>(p, 2, s, waves);
       } else {
-        return launch_staged<DT, BITS, MAXB, STATS>(p, s);
+        // fp32 (HBM-bound): the group spread over the CTA in registers
+        return launch_units<quantize_cta_kernel<DT, BITS, 1, MAXB, STATS>>(p, 4, s, waves);
+      }
+    default:  // G = 4096
+      if constexpr (DT != DT_F32) {
+        return launch_units<quantize_pair_kernel<DT, BITS, MAXB, STATS>>(p, kWarps / 2, s, waves);
+      } else {
+        return launch_units<quantize_cta_kernel<DT, BITS, 2, MAXB, STATS>>(p, 2, s, waves);
       }
   }
 }
