@@ -270,7 +270,8 @@ __device__ __forceinline__ GroupParams group_params(float mn, float mx, float Lf
   mx = __fadd_rn(mx, 0.0f);
   const float range = __fsub_rn(mx, mn);
   p.mn = mn;
-  p.scale = __fdiv_rn(range, Lf);
+  // range / 1 == range exactly (b = 1: the constant folds and the division disappears)
+  p.scale = (Lf == 1.0f) ? range : __fdiv_rn(range, Lf);
   p.inv = (range > 0.0f) ? div_rz_pos(Lf, range) : 0.0f;
   return p;
 }

@@ -86,6 +86,20 @@ bool wide_ok(const void* y, const void* packed) { return aligned(y, 32) && align
 
 namespace gact {
 
+// A launch of one tensor takes the single-tensor kernels (QBatch<1> / DBatch<1>): a 64-byte
+// instead of an 18 KB parameter block, and CTA-uniform bookkeeping. Measured on a 2^27-element
+// bf16 tensor, back to back (tools/launch_cost.py): quantize 65.5 -> 61.7 us at b = 1.
+template <template <int> class PB>
+PB<1> single_of(const PB<kMaxBatch>& p) {
+  PB<1> q;
+  std::memset(&q, 0, sizeof(q));
+  std::memcpy(&q, &p, offsetof(PB<1>, tile_start));
+  q.tile_start[0] = p.tile_start[0];
+  q.tile_start[1] = p.tile_start[1];
+  q.t[0] = p.t[0];
+  return q;
+}
+
 // Items are grouped by (dtype, bits); each class is launched in chunks of <= kMaxBatch
 // items, in input order (the parameter blocks are 16 KB: kept off the stack).
 cudaError_t enqueue_quantize(const QItem* items, int32_t count, int32_t G, cudaStream_t s) {
@@ -115,7 +129,8 @@ cudaError_t enqueue_quantize(const QItem* items, int32_t count, int32_t G, cudaS
       p.count = m;
       p.tile_start[m] = tiles;
       p.tiles_total = tiles;
-      const cudaError_t e = launch_quantize<kMaxBatch>(p, dt, bits, s);
+      const cudaError_t e = m == 1 ? launch_quantize<1>(single_of(p), dt, bits, s)
+                                   : launch_quantize<kMaxBatch>(p, dt, bits, s);
       if (e != cudaSuccess) return e;
     }
   }
@@ -158,7 +173,8 @@ cudaError_t enqueue_dequantize(const DItem* items, int32_t count, int32_t G, cud
       p.count = m;
       p.tile_start[m] = tiles;
       p.tiles_total = tiles;
-      const cudaError_t e = launch_dequantize<kMaxBatch>(p, dt, bits, s);
+      const cudaError_t e = m == 1 ? launch_dequantize<1>(single_of(p), dt, bits, s)
+                                   : launch_dequantize<kMaxBatch>(p, dt, bits, s);
       if (e != cudaSuccess) return e;
     }
   }

@@ -90,8 +90,10 @@ __device__ __forceinline__ void code_chunk_guarded(const QTensor& T, int64_t e, 
   store_unit_guarded<BITS>(T.packed, e, T.nwords, quantize_chunk<BITS>(v, mn, inv, chunk_rand(T, e)));
 }
 
-// One tile of a tensor with G >= 256, full or partial (the group may be short): guarded
-// element loads, warp reduction, per-lane division. The slow generic path, out of line.
+// One tile of a tensor with G >= 256, full or partial (the group may be short): warp
+// reduction, per-lane division, codes; chunks inside the tensor by 16/32-byte loads (the coding
+// pass re-reads them from L1 / L2), the tensor's last chunk element by element. Each chunk's
+// random bytes from its own Philox block (chunk_rand). The slow generic path, out of line.
 template <int DT, int BITS, bool STATS>
 __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g, float Lf,
                                           int lane) {
@@ -99,12 +101,18 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
   float lmn = FLT_MAX, lmx = -FLT_MAX;  // neutral; the tile has at least one element
   for (int c = 0; c < cpl; ++c) {
     const int64_t e = e0 + c * kWarpTile + lane * kChunk;
+    if (e + kChunk <= T.n) {
+      Raw8<DT> raw;
+      load8<DT>(raw, T.x, e);
+      chunk_minmax_raw<DT>(raw, lmn, lmx);
+    } else {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (e + j < T.n) {
-        const float x = load1<DT>(T.x, e + j);
-        lmn = fminf(lmn, x);
-        lmx = fmaxf(lmx, x);
+      for (int j = 0; j < 8; ++j) {
+        if (e + j < T.n) {
+          const float x = load1<DT>(T.x, e + j);
+          lmn = fminf(lmn, x);
+          lmx = fmaxf(lmx, x);
+        }
       }
     }
   }
@@ -117,7 +125,13 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
   if constexpr (!STATS) {
     for (int c = 0; c < cpl; ++c) {
       const int64_t e = e0 + c * kWarpTile + lane * kChunk;
-      if ((e * BITS) / 32 < T.nwords) code_chunk_guarded<DT, BITS>(T, e, gp.mn, gp.inv);
+      if (e + kChunk <= T.n) {
+        Raw8<DT> raw;
+        load8<DT>(raw, T.x, e);
+        store_unit<BITS>(T.packed, e, quantize_chunk_raw<DT, BITS>(raw, gp.mn, gp.inv, chunk_rand(T, e)));
+      } else if ((e * BITS) / 32 < T.nwords) {
+        code_chunk_guarded<DT, BITS>(T, e, gp.mn, gp.inv);
+      }
     }
   }
 }
