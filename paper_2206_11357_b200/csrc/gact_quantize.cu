@@ -179,13 +179,19 @@ static_assert(kWarps * GACT_Q_UNIT <= kTileAlign && kTileAlign % (kWarps * GACT_
               "a CTA unit must divide the tile alignment");
 
 #ifndef GACT_Q_MINB_LOWB
-#define GACT_Q_MINB_LOWB 2  // 2-byte inputs, b <= GACT_Q_LOWB: 2 CTAs per SM (b = 1: +2-3% at G <= 1024; b = 2 neutral, b = 4 -1-5%)
+// 2-byte inputs, b <= GACT_Q_LOWB, single-tensor launches: 2 CTAs per SM (b = 1: +2-3% at
+// G <= 1024; b = 2 neutral, b = 4 -1-5%). Batched launches keep 3 (b = 1 at 2 / 3 CTAs per SM,
+// A/B on one box: ResNet-50 bench quantize 0.853 / 0.860, BERT-large 24 layers 0.793 / 0.801;
+// single 2^28 tensors 119 / 123 us).
+#define GACT_Q_MINB_LOWB 2
 #endif
 #ifndef GACT_Q_LOWB
 #define GACT_Q_LOWB 1
 #endif
 template <int DT, int BITS, int CPL, int MAXB, bool STATS>
-__global__ void __launch_bounds__(kThreads, DT == DT_F32 ? GACT_Q_MINB_F32 : BITS <= GACT_Q_LOWB ? GACT_Q_MINB_LOWB : GACT_Q_MINB)
+__global__ void __launch_bounds__(kThreads, DT == DT_F32                    ? GACT_Q_MINB_F32
+                                           : (BITS <= GACT_Q_LOWB && MAXB == 1) ? GACT_Q_MINB_LOWB
+                                                                                : GACT_Q_MINB)
     quantize_big_kernel(const __grid_constant__ QBatch<MAXB> P) {
   constexpr int U = unit_tiles<DT, CPL>();
   constexpr int TE = CPL * kWarpTile;  // == G

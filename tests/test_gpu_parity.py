@@ -338,6 +338,29 @@ def test_batch_equals_single(gact, G):
         assert torch.equal(y.view(-1), single.decompress().view(-1))
 
 
+@pytest.mark.parametrize("G", GROUPS + [96, 800])
+def test_one_tensor_batch_vs_oracle(gact, orc, G):
+    """A batch call holding one tensor of a (dtype, bits) class launches the single-tensor
+    kernels (gact_host.cu, single_of): codes and decoded values against the oracle, at sizes
+    whose last CTA unit is whole, partial by a few tiles, or partial inside its last tile."""
+    te = max(G, 256)
+    for k, n in enumerate([64 * te, 64 * te * 3 + 5 * te, 64 * te + 3 * te + 77, 1000]):
+        dt = DTYPES[k % 3]
+        b = BITS[k % 4]
+        x = make_input(n, dt, seed=500 + k)
+        s = synth.tensor_seed(41, k)
+        ct = gact.quantize_pack_batch([x], [b], [s], G)[0]
+        y = gact.unpack_dequantize_batch([ct])[0]
+        torch.cuda.synchronize()
+        ref_p, ref_mn, ref_sc = orc.quantize_pack(oracle_input(x), TAGS[dt], G, b, s)
+        assert np.array_equal(host_bits(ct.packed), ref_p)
+        assert np.array_equal(host_bits(ct.group_min), ref_mn.view(np.uint32))
+        assert np.array_equal(host_bits(ct.group_scale), ref_sc.view(np.uint32))
+        ref_y = orc.unpack_dequantize(ref_p, ref_mn, ref_sc, n, G, b, TAGS[dt])
+        d = ulp_distance(host_bits(y), ref_y, 32 if dt == torch.float32 else 16)
+        assert d.max(initial=0) <= 1
+
+
 @pytest.mark.parametrize("dtype", DTYPES, ids=["f32", "bf16", "f16"])
 @pytest.mark.parametrize("G", [2048, 4096])
 def test_batch_large_groups_vs_oracle(gact, orc, dtype, G):
