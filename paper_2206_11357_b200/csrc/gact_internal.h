@@ -102,7 +102,10 @@ inline int64_t quantize_tile_elems(int32_t G) {
 }
 // Each tensor's quantize tile count is rounded up to this, so that a CTA unit (8 warps x up
 // to 8 consecutive tiles) never straddles two tensors of a batch.
-constexpr int64_t kTileAlign = 64;
+#ifndef GACT_TILE_ALIGN
+#define GACT_TILE_ALIGN 128
+#endif
+constexpr int64_t kTileAlign = GACT_TILE_ALIGN;
 inline int64_t quantize_tiles(int64_t n, int32_t G) {
   const int64_t te = quantize_tile_elems(G);
   const int64_t t = (n + te - 1) / te;

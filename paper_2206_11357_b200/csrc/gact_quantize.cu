@@ -6,7 +6,7 @@
 // (8 random bytes = half a Philox4x32-10 block, R3: a lane's chunks in 256-element
 // sub-tiles 2m and 2m + 1 share one block; one 16- or 32-byte coalesced load).
 // Tensors of a batch are concatenated in tile space (QBatch::tile_start), each tensor's
-// tile count rounded up to kTileAlign = 64, so that a CTA UNIT (8 warps x U consecutive
+// tile count rounded up to kTileAlign = 128, so that a CTA UNIT (8 warps x U consecutive
 // tiles) never straddles two tensors. CTAs walk units grid-stride: the active window of a
 // launch is compact in memory, each warp streams U * TE contiguous elements per step, and
 // the unit's bookkeeping (tensor, seed, pointers) is CTA-uniform (single-tensor launches
@@ -137,7 +137,7 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 }
 
 // ---------------------------------------------------------------------------------------
-// G in {256, 512, 1024} (2048 for 2-byte inputs): CPL = G/256 chunks per lane, U = quant_unit<DT>()/CPL tiles per unit,
+// G in {256, 512, 1024} (2048 for 2-byte inputs): CPL = G/256 chunks per lane, U = quant_unit()/CPL tiles per unit,
 // all in registers.
 // Grid = waves x resident CTAs. Several waves (CTAs pick up units dynamically as others
 // retire) beat a persistent grid for the FMA-bound 2-byte inputs (+6% at bf16); fp32 inputs
@@ -154,46 +154,64 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 #ifndef GACT_Q_XRED
 #define GACT_Q_XRED 1  // 2-byte, 8 groups per unit: butterfly reduction of packed (min, -max)
 #endif
-// Chunks (Philox blocks) per lane per CTA unit: 8 for 2-byte inputs (FMA-bound: the unit's
-// 8 blocks share Philox rounds 0-1 and the key schedule / bookkeeping is amortised over 8
-// tiles; ~124 registers, 2 CTAs per SM), 4 for fp32 (HBM-bound; 8 would spill).
+// Chunks (Philox blocks) per lane per CTA unit. 2-byte inputs (issue-bound): 16 -- the unit's
+// 8 Philox blocks share rounds 0-1, and the per-unit work (tensor lookup, key schedule, loop,
+// addresses, the division of each lane's group) is amortised over 16 tiles; 128 registers
+// (12-40 bytes of spills), 2 CTAs per SM. Measured against 8-chunk units at 3 CTAs per SM
+// (80 registers), A/B on one box: ResNet-50 bench quantize 0.845 -> 0.883, BERT-large 24
+// layers 0.771 -> 0.797; single 2^28 bf16 tensors b = 2 / 4 -2.5 / -3% time, b = 8 equal,
+// b = 1 +0.8% -- so single-tensor b = 1 launches keep 8-chunk units (GACT_Q_UNIT_B1S), and
+// so does G = 2048 (16 chunks = 2 groups per warp: b = 2 / 4 / 8 2% / 2% / 1.5% slower).
+// fp32 (HBM-bound): 4 (8 would spill).
 #ifndef GACT_Q_UNIT
-#define GACT_Q_UNIT 8
+#define GACT_Q_UNIT 16
+#endif
+#ifndef GACT_Q_UNIT_B1S
+#define GACT_Q_UNIT_B1S 8
 #endif
 #ifndef GACT_Q_UNIT_F32
 #define GACT_Q_UNIT_F32 4
 #endif
 #ifndef GACT_Q_MINB
-#define GACT_Q_MINB 3  // 2-byte inputs: 3 CTAs per SM (80 registers): ResNet-50 +0.7%, BERT +0.6% vs 2
+#define GACT_Q_MINB 3  // 8-chunk 2-byte units (and the fp32 CTA-wide / 2-byte pair kernels at b = 8): 3 CTAs per SM
+#endif
+#ifndef GACT_Q_MINB_U16
+#define GACT_Q_MINB_U16 2  // 16-chunk 2-byte units: 2 CTAs per SM (128 registers)
 #endif
 #ifndef GACT_Q_MINB_F32
 #define GACT_Q_MINB_F32 2
 #endif
-template <int DT>
-__host__ __device__ constexpr int quant_unit() { return DT == DT_F32 ? GACT_Q_UNIT_F32 : GACT_Q_UNIT; }
-// tiles per warp per unit for G = 256 CPL
-template <int DT, int CPL>
-__host__ __device__ constexpr int unit_tiles() { return quant_unit<DT>() / CPL > 0 ? quant_unit<DT>() / CPL : 1; }
+#ifndef GACT_Q_MINB_LOWB
+// 8-chunk units, b = 1, single-tensor launches: 2 CTAs per SM (+2-3% at G <= 1024 against 3).
+#define GACT_Q_MINB_LOWB 2
+#endif
+// chunks per lane per unit for group size 256 CPL
+template <int DT, int BITS, int MAXB, int CPL>
+__host__ __device__ constexpr int quant_unit() {
+  return DT == DT_F32 ? GACT_Q_UNIT_F32
+         : (CPL == 8 || (BITS == 1 && MAXB == 1)) ? GACT_Q_UNIT_B1S  // G = 2048: one group per warp
+                                                  : GACT_Q_UNIT;
+}
+// tiles per warp per unit
+template <int DT, int BITS, int MAXB, int CPL>
+__host__ __device__ constexpr int unit_tiles() {
+  return quant_unit<DT, BITS, MAXB, CPL>() / CPL > 0 ? quant_unit<DT, BITS, MAXB, CPL>() / CPL : 1;
+}
+template <int DT, int BITS, int MAXB, int CPL>
+__host__ __device__ constexpr int quant_minb() {
+  return DT == DT_F32 ? GACT_Q_MINB_F32
+         : quant_unit<DT, BITS, MAXB, CPL>() >= 16 ? GACT_Q_MINB_U16
+         : (BITS == 1 && MAXB == 1) ? GACT_Q_MINB_LOWB : GACT_Q_MINB;
+}
 static_assert(kWarps * GACT_Q_UNIT <= kTileAlign && kTileAlign % (kWarps * GACT_Q_UNIT) == 0 &&
+              kTileAlign % (kWarps * GACT_Q_UNIT_B1S) == 0 &&
               kWarps * GACT_Q_UNIT_F32 <= kTileAlign && kTileAlign % (kWarps * GACT_Q_UNIT_F32) == 0,
               "a CTA unit must divide the tile alignment");
 
-#ifndef GACT_Q_MINB_LOWB
-// 2-byte inputs, b <= GACT_Q_LOWB, single-tensor launches: 2 CTAs per SM (b = 1: +2-3% at
-// G <= 1024; b = 2 neutral, b = 4 -1-5%). Batched launches keep 3 (b = 1 at 2 / 3 CTAs per SM,
-// A/B on one box: ResNet-50 bench quantize 0.853 / 0.860, BERT-large 24 layers 0.793 / 0.801;
-// single 2^28 tensors 119 / 123 us).
-#define GACT_Q_MINB_LOWB 2
-#endif
-#ifndef GACT_Q_LOWB
-#define GACT_Q_LOWB 1
-#endif
 template <int DT, int BITS, int CPL, int MAXB, bool STATS>
-__global__ void __launch_bounds__(kThreads, DT == DT_F32                    ? GACT_Q_MINB_F32
-                                           : (BITS <= GACT_Q_LOWB && MAXB == 1) ? GACT_Q_MINB_LOWB
-                                                                                : GACT_Q_MINB)
+__global__ void __launch_bounds__(kThreads, quant_minb<DT, BITS, MAXB, CPL>())
     quantize_big_kernel(const __grid_constant__ QBatch<MAXB> P) {
-  constexpr int U = unit_tiles<DT, CPL>();
+  constexpr int U = unit_tiles<DT, BITS, MAXB, CPL>();
   constexpr int TE = CPL * kWarpTile;  // == G
   constexpr int CU = kWarps * U;       // tiles per CTA unit (divides kTileAlign)
   const int lane = threadIdx.x & 31;
@@ -251,8 +269,8 @@ __global__ void __launch_bounds__(kThreads, DT == DT_F32                    ? GA
       // (mn, inv) come back by two shuffles from lane k << (5 - log2 U). For U = 8 (G = 256):
       // 9 shuffles + 9 HMNMX2 for all 8 groups, where one CREDUX pair per group needs 16
       // CREDUX + 16 uniform-to-vector moves + 14 selects.
-      constexpr int LU = U == 8 ? 3 : U == 4 ? 2 : U == 2 ? 1 : 0;
-      static_assert((1 << LU) == U, "U is a power of two <= 8");
+      constexpr int LU = U == 16 ? 4 : U == 8 ? 3 : U == 4 ? 2 : U == 2 ? 1 : 0;
+      static_assert((1 << LU) == U, "U is a power of two <= 16");
       constexpr int SH = 5 - LU;
       uint32_t p[U];
 #pragma unroll
@@ -754,16 +772,16 @@ cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
     case 7:
       return launch_persistent<quantize_small_kernel<DT, BITS, MAXB, STATS, 7>>(p, small_unit<DT, 7>(), s, waves);
     case 8:
-      return launch_persistent<quantize_big_kernel<DT, BITS, 1, MAXB, STATS>>(p, unit_tiles<DT, 1>(), s, waves);
+      return launch_persistent<quantize_big_kernel<DT, BITS, 1, MAXB, STATS>>(p, unit_tiles<DT, BITS, MAXB, 1>(), s, waves);
     case 9:
-      return launch_persistent<quantize_big_kernel<DT, BITS, 2, MAXB, STATS>>(p, unit_tiles<DT, 2>(), s, waves);
+      return launch_persistent<quantize_big_kernel<DT, BITS, 2, MAXB, STATS>>(p, unit_tiles<DT, BITS, MAXB, 2>(), s, waves);
     case 10:
-      return launch_persistent<quantize_big_kernel<DT, BITS, 4, MAXB, STATS>>(p, unit_tiles<DT, 4>(), s, waves);
+      return launch_persistent<quantize_big_kernel<DT, BITS, 4, MAXB, STATS>>(p, unit_tiles<DT, BITS, MAXB, 4>(), s, waves);
     case 11:
       if constexpr (DT != DT_F32) {
         // 2-byte inputs: one group per warp, 8 chunks per lane, all in registers (the 8-chunk
         // unit of G = 256 with U = 1 tile), read once.
-        return launch_persistent<quantize_big_kernel<DT, BITS, 8, MAXB, STATS>>(p, unit_tiles<DT, 8>(), s, waves);
+        return launch_persistent<quantize_big_kernel<DT, BITS, 8, MAXB, STATS>>(p, unit_tiles<DT, BITS, MAXB, 8>(), s, waves);
       } else {
         // fp32 (HBM-bound): the group spread over the CTA in registers
         return launch_units<quantize_cta_kernel<DT, BITS, 1, MAXB, STATS>>(p, 4, s, waves);

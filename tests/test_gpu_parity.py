@@ -179,9 +179,10 @@ def test_c1_config(gact, orc):
 @pytest.mark.parametrize("G", GROUPS)
 def test_quantize_dequantize_parity(gact, orc, dtype, bits, G):
     TE = max(G, 256)
-    # two full CTA units (8192 elements: the unguarded fast path of every kernel), then
-    # several tiles, a ragged tail and a partial chunk (the guarded path)
-    n = 2 * 8192 + 3 * TE + 8 * 5 + 3
+    # two of the largest CTA units (32768 elements: 8 warps x 16 chunks x 256 for 2-byte
+    # inputs; the unguarded fast path of every kernel), then several tiles, a ragged tail and
+    # a partial chunk (the guarded path)
+    n = 2 * 32768 + 3 * TE + 8 * 5 + 3
     x = make_input(n, dtype, seed=G * 10 + bits)
     ct, ref = check_quantize(gact, orc, x, G, bits, seed=0xABCDEF0123456789 ^ (G * bits))
     for ydt in DTYPES:
@@ -239,7 +240,7 @@ def test_edge_groups_every_kernel(gact, orc, dtype, bits, G):
     """Subnormal, signed-zero and near-overflow groups through every kernel (all G, every b,
     every dtype), full units and a ragged tail: codes bit-exact, decoded values <= 1 ulp."""
     TE = max(G, 256)
-    n = 2 * 8192 + 8 * TE + 77
+    n = 2 * 32768 + 8 * TE + 77  # two of the largest CTA units (2-byte: 32768 elements), then a tail
     x = make_input(n, dtype, seed=G * 7 + bits, kind="edge2", group=G)
     hb = host_bits(x)
     if dtype != torch.float32:  # the inputs really are 2-byte subnormals / -0 / near-max
@@ -366,7 +367,7 @@ def test_one_tensor_batch_vs_oracle(gact, orc, G):
 def test_batch_large_groups_vs_oracle(gact, orc, dtype, G):
     """Batched launches at G = 2048 / 4096 (the fp32 CTA-wide kernel, the 2-byte register
     and shared-memory-stage kernels) against the oracle, tensor by tensor. 40 ragged tensors
-    per launch: every tensor ends in a partial group and is padded to 64 tiles, so guarded
+    per launch: every tensor ends in a partial group and is padded to 128 tiles, so guarded
     units interleave with full ones inside one CTA's sequence, and the launch has more units
     than its grid (CTAs wrap across tensor tails)."""
     rng = np.random.default_rng(G + TAGS[dtype])
@@ -466,7 +467,7 @@ def test_threshold_ties(gact, orc, bits, G):
     unguarded fast path (>= 2 CTA units) and a ragged tail."""
     import tie_cases
     seed = 0x5EED0000 + G * 16 + bits
-    ng = max(2 * 8192 // G, 2) + 3
+    ng = max(2 * 32768 // G, 2) + 3
     xh, want = tie_cases.tie_groups(ng, G, bits, seed, orc.rand8, np.random.default_rng(G + bits))
     xh = xh[: xh.size - 5]  # ragged tail: the last group is short
     want = want[: xh.size]
