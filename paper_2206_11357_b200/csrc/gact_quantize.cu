@@ -11,18 +11,19 @@
 // launch is compact in memory, each warp streams U * TE contiguous elements per step, and
 // the unit's bookkeeping (tensor, seed, pointers) is CTA-uniform (single-tensor launches
 // keep it in the uniform datapath; batched launches index the descriptor table per unit).
-//  * G in {256, 512, 1024} (and 2048 for 2-byte inputs): one tile == one group, reduced in
-//    registers, coded from the same registers, written once: x is read exactly once. The
-//    U x CPL / 2 (4 for 2-byte inputs, 2 for fp32) Philox blocks of a lane are computed
-//    while the unit's loads are in flight (they depend only on (seed, element index)), with
-//    their rounds 0-1 shared (philox4x32_10_xn). Min / max: 2-byte inputs at G = 256 (8
-//    groups per unit) fold packed (min, -max) pairs and reduce all 8 groups with one
-//    recursive-halving butterfly (GACT_Q_XRED); otherwise FMNMX3 in-thread and one CREDUX
-//    per group for min and max. The U groups' divisions run on U lanes and are broadcast
-//    with shuffles.
+//  * G in {256, ..., 4096} (2048 and 4096: 2-byte inputs only): one tile == one group, reduced
+//    in registers, coded from the same registers, written once: x is read exactly once. A
+//    lane holds 16 chunks per unit for 2-byte inputs (U = 16 / CPL tiles; 8 chunks for
+//    G = 2048 and for single-tensor b = 1 launches), 4 for fp32. The lane's Philox blocks (two
+//    chunks per block) are computed while the unit's loads are in flight (they depend only on
+//    (seed, element index)), with their rounds 0-1 shared (philox4x32_10_xn). Min / max:
+//    2-byte units of U >= 2 groups fold packed (min, -max) pairs and reduce all U groups with
+//    one recursive-halving butterfly (GACT_Q_XRED), each lane computes one group's division,
+//    and the groups' (mn, inv) reach the lanes through shared memory; otherwise FMNMX3
+//    in-thread, one CREDUX per group for min and max, divisions on U lanes, shuffles.
 //  * G in {32, 64, 128}: a tile holds 256/G groups of G/8 lanes; segmented shuffles.
-//  * G = 4096 (2-byte inputs): the group spans a warp pair's registers; G in {2048, 4096}
-//    fp32: the group spans the CTA's registers (one HBM read either way).
+//  * G in {2048, 4096}, fp32: the group spans the CTA's registers (one HBM read).
+//  * G not a power of two: a warp per group, two passes (the second from L1 / L2).
 // A tensor's last tile may be partial (n % TE != 0): it takes the guarded generic path.
 #include <cfloat>
 
@@ -168,6 +169,9 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 // layers 0.771 -> 0.797; single 2^28 bf16 tensors b = 2 / 4 -2.5 / -3% time, b = 8 equal,
 // b = 1 +0.8% -- so single-tensor b = 1 launches keep 8-chunk units (GACT_Q_UNIT_B1S), and
 // so does G = 2048 (16 chunks = 2 groups per warp: b = 2 / 4 / 8 2% / 2% / 1.5% slower).
+// G = 4096 (2-byte): 16 chunks = one group per warp; replaced a warp-pair kernel (8 chunks
+// per lane, the pair's min / max through shared memory behind a named barrier): bf16 2^28
+// b = 1 / 2 / 4 117.2 / 116.9 / 119.8 -> 112.0 / 111.9 / 113.2 us, b = 8 equal.
 // fp32 (HBM-bound): 4 (8 would spill).
 #ifndef GACT_Q_UNIT
 #define GACT_Q_UNIT 16
@@ -179,7 +183,7 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 #define GACT_Q_UNIT_F32 4
 #endif
 #ifndef GACT_Q_MINB
-#define GACT_Q_MINB 3  // 8-chunk 2-byte units (and the fp32 CTA-wide / 2-byte pair kernels at b = 8): 3 CTAs per SM
+#define GACT_Q_MINB 3  // 8-chunk 2-byte units and the fp32 CTA-wide kernel: 3 CTAs per SM
 #endif
 #ifndef GACT_Q_MINB_U16
 #define GACT_Q_MINB_U16 2  // 16-chunk 2-byte units: 2 CTAs per SM (128 registers)
@@ -195,6 +199,7 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 template <int DT, int BITS, int MAXB, int CPL>
 __host__ __device__ constexpr int quant_unit() {
   return DT == DT_F32 ? GACT_Q_UNIT_F32
+         : CPL == 16 ? 16                                            // G = 4096: one group per warp
          : (CPL == 8 || (BITS == 1 && MAXB == 1)) ? GACT_Q_UNIT_B1S  // G = 2048: one group per warp
                                                   : GACT_Q_UNIT;
 }
@@ -370,75 +375,6 @@ __global__ void __launch_bounds__(kThreads, quant_minb<DT, BITS, MAXB, CPL>())
           store_unit_at<BITS>(out + ((k * TE + c * kWarpTile) * BITS) / 8,
                               quantize_chunk_raw<DT, BITS>(raw[k][c], mn, inv, rnd[k][c]));
       }
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------------------
-// G = 4096, 2-byte inputs: a group spans a warp pair (2m, 2m + 1), 2048 elements = 8 chunks per
-// lane each, all in registers (x read once, no stage). Each warp reduces its half with CREDUX;
-// the pair's two (min, max) meet in shared memory behind a 64-thread named barrier (one per
-// pair and unit; double-buffered by unit parity, so the next unit's write cannot overtake the
-// partner's read). A warp's 8 chunks are 4 whole 512-element spans: its 4 Philox blocks
-// (R3) are used in full, rounds 0-1 shared.
-#ifndef GACT_Q_PAIR_MINB
-#define GACT_Q_PAIR_MINB 2  // b <= 4 (b = 8: GACT_Q_MINB)
-#endif
-template <int DT, int BITS, int MAXB, bool STATS>
-__global__ void __launch_bounds__(kThreads, BITS >= 8 ? GACT_Q_MINB : GACT_Q_PAIR_MINB)
-    quantize_pair_kernel(const __grid_constant__ QBatch<MAXB> P) {
-  constexpr int CPL = 8;
-  constexpr int WE = CPL * kWarpTile;  // elements of a group per warp
-  constexpr int TE = 2 * WE;           // == G
-  constexpr int U = kWarps / 2;        // groups per CTA unit
-  __shared__ float2 red[2][U][2];      // [parity][pair][warp of the pair] = (min, max)
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int pair = warp >> 1, half = warp & 1;
-  const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
-  const int64_t cunits = P.tiles_total / U;  // a quantize tile is one group here
-  int cur = first_cursor(P, (int64_t)blockIdx.x * U), par = 0;
-  for (int64_t cu = blockIdx.x; cu < cunits; cu += gridDim.x) {
-    cur = advance_cursor(P, cur, cu * U);
-    const QTensor& T = P.t[cur];
-    const int64_t e_unit = (cu * U - P.tile_start[cur]) * TE;
-    if (e_unit + U * TE > T.n) {  // CTA-uniform: the tensor's last unit, warp k codes group k
-      if (warp < U && e_unit + warp * TE < T.n)
-        tile_generic<DT, BITS, STATS>(T, e_unit + warp * TE, P.log2g, Lf, lane);
-      continue;  // no barrier, `par` unchanged
-    }
-    const int64_t e_lane = e_unit + pair * TE + half * WE + lane * kChunk;
-    Raw8<DT> raw[CPL];
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) load8<DT>(raw[c], T.x, e_lane + c * kWarpTile);
-    uint2 rnd[CPL];
-    if constexpr (!STATS) {
-      uint4 r4[CPL / 2];
-      philox4x32_10_xn<CPL / 2>(rand_block(T, e_lane), (uint32_t)T.seed, (uint32_t)(T.seed >> 32), r4);
-#pragma unroll
-      for (int c = 0; c < CPL; ++c)
-        rnd[c] = (c & 1) ? make_uint2(r4[c >> 1].z, r4[c >> 1].w) : make_uint2(r4[c >> 1].x, r4[c >> 1].y);
-    }
-    float lmn = FLT_MAX, lmx = -FLT_MAX;
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) chunk_minmax_raw<DT>(raw[c], lmn, lmx);
-    lmn = warp_min(lmn);
-    lmx = warp_max(lmx);
-    if (lane == 0) red[par][pair][half] = make_float2(lmn, lmx);
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
-    const float2 o = red[par][pair][half ^ 1];
-    par ^= 1;
-    const GroupParams gp = group_params(fminf(lmn, o.x), fmaxf(lmx, o.y), Lf);
-    if (half == 0 && lane == 0) {
-      const int64_t g = (e_unit >> P.log2g) + pair;
-      T.group_min[g] = gp.mn;
-      T.group_scale[g] = gp.scale;
-    }
-    if constexpr (!STATS) {
-      unsigned char* out = reinterpret_cast<unsigned char*>(T.packed) + (e_lane * BITS) / 8;
-#pragma unroll
-      for (int c = 0; c < CPL; ++c)
-        store_unit_at<BITS>(out + (c * kWarpTile * BITS) / 8, quantize_chunk_raw<DT, BITS>(raw[c], gp.mn, gp.inv, rnd[c]));
     }
   }
 }
@@ -811,7 +747,8 @@ cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
       }
     default:  // G = 4096
       if constexpr (DT != DT_F32) {
-        return launch_units<quantize_pair_kernel<DT, BITS, MAXB, STATS>>(p, kWarps / 2, s, waves);
+        // 2-byte inputs: one group per warp, 16 chunks per lane in registers, read once
+        return launch_persistent<quantize_big_kernel<DT, BITS, 16, MAXB, STATS>>(p, unit_tiles<DT, BITS, MAXB, 16>(), s, waves);
       } else {
         return launch_units<quantize_cta_kernel<DT, BITS, 2, MAXB, STATS>>(p, 2, s, waves);
       }
