@@ -297,24 +297,44 @@ struct PackedUnit {
   uint32_t lo, hi;  // hi used only for BITS == 8 (64-bit unit)
 };
 
+#ifndef GACT_MAGIC_OFFSETS
+#define GACT_MAGIC_OFFSETS 1
+#endif
+// Integer offset m_j added to element j's magic (2^23 - 128 + m_j: bits(w_j) = 0x4B00_0000 + m_j
+// + q_j, still on the integer grid of [2^23, 2^24) and below 2^24), chosen so that the offsets
+// cancel in the packed sum: sum_j (0x4B00_0000 + m_j) << (b j) == 0 (mod 2^32), which saves the
+// correction add per chunk. Each m_j is a multiple of 2^16, so m_j << (b j) lies above the code
+// bits. b = 4: 0x4B00_0000 + 0xB500_0000; b = 2: 0xE700_0000 + (0x64_0000 << 6); b = 1:
+// 0xB500_0000 + (0x2E_0000 << 6) + (0x7F_0000 << 7).
 template <int BITS>
-__device__ __forceinline__ constexpr uint32_t magic_sum(int first, int count) {
+__host__ __device__ constexpr uint32_t magic_off(int j) {
+  if (!GACT_MAGIC_OFFSETS) return 0;
+  return BITS == 4 ? (j == 1 ? 0x500000u : 0u)
+       : BITS == 2 ? (j == 3 ? 0x640000u : 0u)
+       : BITS == 1 ? (j == 6 ? 0x2E0000u : j == 7 ? 0x7F0000u : 0u) : 0u;
+}
+template <int BITS>
+__host__ __device__ constexpr uint32_t magic_sum(int first, int count) {
   uint32_t s = 0;
-  for (int j = 0; j < count; ++j) s += 0x4B000000u << ((first + j) * BITS);
+  for (int j = first; j < first + count; ++j) s += (0x4B000000u + magic_off<BITS>(j)) << (j * BITS);
   return s;
 }
+static_assert(!GACT_MAGIC_OFFSETS || (magic_sum<1>(0, 8) == 0 && magic_sum<2>(0, 8) == 0 && magic_sum<4>(0, 8) == 0),
+              "the magic offsets cancel in the packed sum");
 
 // w_j (= 0x4B00_0000 + q_j) of the pair (d_lo, d_hi) whose random bytes are bytes SEL and
 // SEL + 1 of Philox word rw. (Building c in the integer pipe instead -- funnel shift + lop3
 // -- was measured slower in round 1: it overloads the ALU pipe that the Philox xors and byte
 // permutes use.)
-template <int SEL>
+template <int SEL, int BITS, int J>
 __device__ __forceinline__ void code_pair(f2_t d2, f2_t inv2, uint32_t rw, uint32_t& w_lo,
                                           uint32_t& w_hi) {
   static_assert(SEL == 0 || SEL == 2, "a pair's bytes are 0-1 or 2-3 of its word");
   const uint32_t clo = __byte_perm(rw, 0x43000080u, 0x7604 | (SEL << 4));        // 128 + (2k+1) 2^-9
   const uint32_t chi = __byte_perm(rw, 0x43000080u, 0x7604 | ((SEL + 1) << 4));
-  const f2_t magic = f2_make(8388608.0f - 128.0f, 8388608.0f - 128.0f);
+  // elements J, J + 1 of the chunk: 2^23 - 128 + m_j (exact: integers below 2^24)
+  const f2_t magic = f2_make(8388608.0f - 128.0f + (float)magic_off<BITS>(J),
+                             8388608.0f - 128.0f + (float)magic_off<BITS>(J + 1));
   f2_split_bits(f2_add_rm(f2_fma_rm(d2, inv2, f2_bits(clo, chi)), magic), w_lo, w_hi);
 }
 
@@ -353,10 +373,10 @@ template <int BITS>
 __device__ __forceinline__ PackedUnit<BITS> code_and_pack(const f2_t d2[4], float inv, uint2 r) {
   const f2_t inv2 = f2_make(inv, inv);
   uint32_t w[8];
-  code_pair<0>(d2[0], inv2, r.x, w[0], w[1]);
-  code_pair<2>(d2[1], inv2, r.x, w[2], w[3]);
-  code_pair<0>(d2[2], inv2, r.y, w[4], w[5]);
-  code_pair<2>(d2[3], inv2, r.y, w[6], w[7]);
+  code_pair<0, BITS, 0>(d2[0], inv2, r.x, w[0], w[1]);
+  code_pair<2, BITS, 2>(d2[1], inv2, r.x, w[2], w[3]);
+  code_pair<0, BITS, 4>(d2[2], inv2, r.y, w[4], w[5]);
+  code_pair<2, BITS, 6>(d2[3], inv2, r.y, w[6], w[7]);
   return pack_codes<BITS>(w);
 }
 
