@@ -91,6 +91,8 @@ namespace gact {
 // bf16 tensor, back to back (tools/launch_cost.py): quantize 65.5 -> 61.7 us at b = 1.
 template <template <int> class PB>
 PB<1> single_of(const PB<kMaxBatch>& p) {
+  static_assert(offsetof(PB<1>, tile_start) == offsetof(PB<kMaxBatch>, tile_start),
+                "the scalar prefix of the parameter block does not depend on MAXB");
   PB<1> q;
   std::memset(&q, 0, sizeof(q));
   std::memcpy(&q, &p, offsetof(PB<1>, tile_start));
