@@ -369,9 +369,41 @@ __device__ __forceinline__ PackedUnit<BITS> pack_codes(const uint32_t w[8]) {
 // (Coding each pair's odd element at scale 2^b and packing by two exact fp32 adds per pair
 // plus 3 byte permutes -- moving the packing off the FMA-heavy pipe -- was measured slower
 // in round 1: bf16 2^28, b = 1 / 2 / 4: 195 / 200 / 183 us vs 175 / 179 / 171.)
-template <int BITS>
+// BYTE2 (b <= 2): codes from byte 2 of the FFMA2.RM result, gathered by byte permutes and two
+// multiplies -- taken by the G = 256 2-byte kernel (A/B: b = 2 +0.7%, ResNet-50 quantize +1%,
+// b = 1 equal); at G = 64 / 1024 / 4096 it measured 1-2.5% slower, so the others keep the
+// integerising add and the shift-add packing.
+template <int BITS, bool BYTE2 = false>
 __device__ __forceinline__ PackedUnit<BITS> code_and_pack(const f2_t d2[4], float inv, uint2 r) {
   const f2_t inv2 = f2_make(inv, inv);
+  if constexpr (BYTE2 && BITS <= 2) {
+    // v_j = fma.rm(d_j, inv, 128 + u_j) lies in [128, 128 + 2^b): bits(v_j) = 0x4300_0000 +
+    // floor((v_j - 128) 2^16), so byte 2 of bits(v_j) is q_j (no integerising add). Gather the
+    // eight byte-2 values into A = [q0, q1, q2, q3], B = [q4, .., q7] (6 byte permutes), then
+    // one multiply per word moves its four b-bit codes into byte 3, the cross products of the
+    // multiply landing below bit 24 in disjoint fields (b = 1: A * 0x01020408 puts q_i at bit
+    // 24 + i, B * 0x10204080 at bit 28 + i, their sum is the code byte; b = 2: A * 0x01041040
+    // puts q_i at bits 24 + 2i, likewise B, and one permute joins the two bytes).
+    uint32_t v[8];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const uint32_t rw = p < 2 ? r.x : r.y;
+      const int sel = (p & 1) * 2;
+      const uint32_t clo = __byte_perm(rw, 0x43000080u, 0x7604 | (sel << 4));
+      const uint32_t chi = __byte_perm(rw, 0x43000080u, 0x7604 | ((sel + 1) << 4));
+      f2_split_bits(f2_fma_rm(d2[p], inv2, f2_bits(clo, chi)), v[2 * p], v[2 * p + 1]);
+    }
+    const uint32_t A = __byte_perm(__byte_perm(v[0], v[1], 0x0062), __byte_perm(v[2], v[3], 0x0062), 0x5410);
+    const uint32_t B = __byte_perm(__byte_perm(v[4], v[5], 0x0062), __byte_perm(v[6], v[7], 0x0062), 0x5410);
+    PackedUnit<BITS> out;
+    out.hi = 0;
+    if constexpr (BITS == 1) {
+      out.lo = (A * 0x01020408u + B * 0x10204080u) >> 24;
+    } else {
+      out.lo = __byte_perm(A * 0x01041040u, B * 0x01041040u, 0x0073);
+    }
+    return out;
+  }
   uint32_t w[8];
   code_pair<0, BITS, 0>(d2[0], inv2, r.x, w[0], w[1]);
   code_pair<2, BITS, 2>(d2[1], inv2, r.x, w[2], w[3]);
@@ -393,7 +425,7 @@ __device__ __forceinline__ PackedUnit<BITS> quantize_chunk(const float v[8], flo
 
 // Straight from the loaded chunk. bf16 / f16: d = x - mn by the mixed-precision subtract
 // (sub.rn.f32.bf16 / .f16: exact widening, one binary32 rounding) on each half-word.
-template <int DT, int BITS>
+template <int DT, int BITS, bool BYTE2 = false>
 __device__ __forceinline__ PackedUnit<BITS> quantize_chunk_raw(const Raw8<DT>& raw, float mn,
                                                                float inv, uint2 r) {
   if constexpr (DT == DT_F32) {
@@ -417,7 +449,7 @@ __device__ __forceinline__ PackedUnit<BITS> quantize_chunk_raw(const Raw8<DT>& r
       }
       d2[p] = f2_make(dlo, dhi);
     }
-    return code_and_pack<BITS>(d2, inv, r);
+    return code_and_pack<BITS, BYTE2>(d2, inv, r);
   }
 }
 

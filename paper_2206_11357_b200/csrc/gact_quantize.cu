@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, quant_minb<DT, BITS, MAXB, CPL>())
 #pragma unroll
         for (int c = 0; c < CPL; ++c)
           store_unit_at<BITS>(out + ((k * TE + c * kWarpTile) * BITS) / 8,
-                              quantize_chunk_raw<DT, BITS>(raw[k][c], mn, inv, rnd[k][c]));
+                              quantize_chunk_raw<DT, BITS, CPL == 1>(raw[k][c], mn, inv, rnd[k][c]));
       }
 #if GACT_Q_SMEMBC
       __syncwarp();  // every lane has read bc[warp] before the next unit writes it
