@@ -297,6 +297,9 @@ struct PackedUnit {
   uint32_t lo, hi;  // hi used only for BITS == 8 (64-bit unit)
 };
 
+#ifndef GACT_BYTE2_MAXB
+#define GACT_BYTE2_MAXB 4  // byte-2 codes up to this b (G = 256 kernel; b = 8 packs by byte permutes anyway)
+#endif
 #ifndef GACT_MAGIC_OFFSETS
 #define GACT_MAGIC_OFFSETS 1
 #endif
@@ -369,21 +372,22 @@ __device__ __forceinline__ PackedUnit<BITS> pack_codes(const uint32_t w[8]) {
 // (Coding each pair's odd element at scale 2^b and packing by two exact fp32 adds per pair
 // plus 3 byte permutes -- moving the packing off the FMA-heavy pipe -- was measured slower
 // in round 1: bf16 2^28, b = 1 / 2 / 4: 195 / 200 / 183 us vs 175 / 179 / 171.)
-// BYTE2 (b <= 2): codes from byte 2 of the FFMA2.RM result, gathered by byte permutes and two
-// multiplies -- taken by the G = 256 2-byte kernel (A/B: b = 2 +0.7%, ResNet-50 quantize +1%,
-// b = 1 equal); at G = 64 / 1024 / 4096 it measured 1-2.5% slower, so the others keep the
-// integerising add and the shift-add packing.
+// BYTE2 (b <= 4): codes from byte 2 of the FFMA2.RM result, gathered by byte permutes and
+// packed by one or two multiplies -- taken by the G = 256 2-byte kernel (A/B: b = 4 +2.7%, b = 2
+// +0.7%, b = 1 +1%, ResNet-50 quantize +1-2%); at G = 64 / 1024 / 4096 it measured 1-2.5%
+// slower (b <= 2), so the others keep the integerising add and the shift-add packing.
 template <int BITS, bool BYTE2 = false>
 __device__ __forceinline__ PackedUnit<BITS> code_and_pack(const f2_t d2[4], float inv, uint2 r) {
   const f2_t inv2 = f2_make(inv, inv);
-  if constexpr (BYTE2 && BITS <= 2) {
+  if constexpr (BYTE2 && BITS <= GACT_BYTE2_MAXB) {
     // v_j = fma.rm(d_j, inv, 128 + u_j) lies in [128, 128 + 2^b): bits(v_j) = 0x4300_0000 +
     // floor((v_j - 128) 2^16), so byte 2 of bits(v_j) is q_j (no integerising add). Gather the
-    // eight byte-2 values into A = [q0, q1, q2, q3], B = [q4, .., q7] (6 byte permutes), then
-    // one multiply per word moves its four b-bit codes into byte 3, the cross products of the
-    // multiply landing below bit 24 in disjoint fields (b = 1: A * 0x01020408 puts q_i at bit
-    // 24 + i, B * 0x10204080 at bit 28 + i, their sum is the code byte; b = 2: A * 0x01041040
-    // puts q_i at bits 24 + 2i, likewise B, and one permute joins the two bytes).
+    // eight byte-2 values into two words by 6 byte permutes. b = 4: A = [q0, q2, q4, q6],
+    // B = [q1, q3, q5, q7], A + 16 B is the packed word. b <= 2: A = [q0, q1, q2, q3],
+    // B = [q4, .., q7], and one multiply per word moves its four b-bit codes into byte 3, the
+    // cross products landing below bit 24 in disjoint fields (b = 1: A * 0x01020408 puts q_i at
+    // bit 24 + i, B * 0x10204080 at bit 28 + i, their sum is the code byte; b = 2:
+    // A * 0x01041040 puts q_i at bits 24 + 2i, likewise B, and one permute joins the bytes).
     uint32_t v[8];
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
@@ -393,10 +397,16 @@ __device__ __forceinline__ PackedUnit<BITS> code_and_pack(const f2_t d2[4], floa
       const uint32_t chi = __byte_perm(rw, 0x43000080u, 0x7604 | ((sel + 1) << 4));
       f2_split_bits(f2_fma_rm(d2[p], inv2, f2_bits(clo, chi)), v[2 * p], v[2 * p + 1]);
     }
-    const uint32_t A = __byte_perm(__byte_perm(v[0], v[1], 0x0062), __byte_perm(v[2], v[3], 0x0062), 0x5410);
-    const uint32_t B = __byte_perm(__byte_perm(v[4], v[5], 0x0062), __byte_perm(v[6], v[7], 0x0062), 0x5410);
     PackedUnit<BITS> out;
     out.hi = 0;
+    if constexpr (BITS == 4) {  // even codes in A, odd codes in B: byte i = q_2i | q_2i+1 << 4
+      const uint32_t A = __byte_perm(__byte_perm(v[0], v[2], 0x0062), __byte_perm(v[4], v[6], 0x0062), 0x5410);
+      const uint32_t B = __byte_perm(__byte_perm(v[1], v[3], 0x0062), __byte_perm(v[5], v[7], 0x0062), 0x5410);
+      out.lo = B * 16u + A;
+      return out;
+    }
+    const uint32_t A = __byte_perm(__byte_perm(v[0], v[1], 0x0062), __byte_perm(v[2], v[3], 0x0062), 0x5410);
+    const uint32_t B = __byte_perm(__byte_perm(v[4], v[5], 0x0062), __byte_perm(v[6], v[7], 0x0062), 0x5410);
     if constexpr (BITS == 1) {
       out.lo = (A * 0x01020408u + B * 0x10204080u) >> 24;
     } else {
