@@ -152,6 +152,9 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 #ifndef GACT_QS_MINB
 #define GACT_QS_MINB 3  // small-G kernel: minimum resident CTAs per SM (register cap)
 #endif
+#ifndef GACT_BYTE2_CPL
+#define GACT_BYTE2_CPL 2  // byte-2 codes (code_and_pack) for G <= 256 * this: G = 512 +1.5-3% at every b; G = 1024 mixed (-0.7% .. +1%), not taken
+#endif
 #ifndef GACT_Q_SMEMBC
 // 2-byte units: the groups' (mn, inv) reach the lanes through shared memory (one 8-byte
 // broadcast load per tile) instead of two shuffles per tile. A/B: single 2^28 bf16 G = 256
@@ -333,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, quant_minb<DT, BITS, MAXB, CPL>())
 #pragma unroll
         for (int c = 0; c < CPL; ++c)
           store_unit_at<BITS>(out + ((k * TE + c * kWarpTile) * BITS) / 8,
-                              quantize_chunk_raw<DT, BITS, CPL == 1>(raw[k][c], mn, inv, rnd[k][c]));
+                              quantize_chunk_raw<DT, BITS, CPL <= GACT_BYTE2_CPL>(raw[k][c], mn, inv, rnd[k][c]));
       }
 #if GACT_Q_SMEMBC
       __syncwarp();  // every lane has read bc[warp] before the next unit writes it
