@@ -155,6 +155,9 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 #ifndef GACT_BYTE2_CPL
 #define GACT_BYTE2_CPL 2  // byte-2 codes (code_and_pack) for G <= 256 * this: G = 512 +1.5-3% at every b; G = 1024 mixed (-0.7% .. +1%), not taken
 #endif
+#ifndef GACT_BYTE2_MIX
+#define GACT_BYTE2_MIX 4  // G = 256: every 4th chunk packs by shift-add (0: every chunk byte-2)
+#endif
 #ifndef GACT_Q_SMEMBC
 // 2-byte units: the groups' (mn, inv) reach the lanes through shared memory (one 8-byte
 // broadcast load per tile) instead of two shuffles per tile. A/B: single 2^28 bf16 G = 256
@@ -334,9 +337,16 @@ __global__ void __launch_bounds__(kThreads, quant_minb<DT, BITS, MAXB, CPL>())
         const float mn = __shfl_sync(kFull, gp.mn, src);
 #endif
 #pragma unroll
-        for (int c = 0; c < CPL; ++c)
-          store_unit_at<BITS>(out + ((k * TE + c * kWarpTile) * BITS) / 8,
-                              quantize_chunk_raw<DT, BITS, CPL <= GACT_BYTE2_CPL>(raw[k][c], mn, inv, rnd[k][c]));
+        for (int c = 0; c < CPL; ++c) {
+          // G = 256: every GACT_BYTE2_MIX-th chunk takes the shift-add packing (FMA pipes)
+          // instead of the byte-2 gather (ALU pipe), balancing the two (A/B, 1 in 4: b = 1
+          // +1.5%, ResNet-50 quantize +1%; 1 in 2 slower; at G = 512 the mix measured slower)
+          constexpr int MIX = CPL == 1 ? GACT_BYTE2_MIX : 0;
+          const bool b2 = CPL <= GACT_BYTE2_CPL && (MIX == 0 || (k * CPL + c) % (MIX > 0 ? MIX : 1) != MIX - 1);
+          unsigned char* o = out + ((k * TE + c * kWarpTile) * BITS) / 8;
+          if (b2) store_unit_at<BITS>(o, quantize_chunk_raw<DT, BITS, true>(raw[k][c], mn, inv, rnd[k][c]));
+          else store_unit_at<BITS>(o, quantize_chunk_raw<DT, BITS, false>(raw[k][c], mn, inv, rnd[k][c]));
+        }
       }
 #if GACT_Q_SMEMBC
       __syncwarp();  // every lane has read bc[warp] before the next unit writes it
