@@ -165,7 +165,7 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 #define GACT_Q_SMEMBC 1
 #endif
 #ifndef GACT_Q_XRED
-#define GACT_Q_XRED 1  // 2-byte, 8 groups per unit: butterfly reduction of packed (min, -max)
+#define GACT_Q_XRED 1  // 2-byte units of U >= 2 groups: butterfly reduction of packed (min, -max)
 #endif
 // Chunks (Philox blocks) per lane per CTA unit. 2-byte inputs (issue-bound): 16 -- the unit's
 // 8 Philox blocks share rounds 0-1, and the per-unit work (tensor lookup, key schedule, loop,
@@ -286,9 +286,10 @@ __global__ void __launch_bounds__(kThreads, quant_minb<DT, BITS, MAXB, CPL>())
       // the tiles a lane keeps (the lane with bit `mask` set keeps the upper half and sends the
       // lower), the remaining levels finish the reduction of the one left: lane l ends with
       // group t(l) = (l >> (5 - log2 U)) & (U - 1), computes its parameters, and group k's
-      // (mn, inv) come back by two shuffles from lane k << (5 - log2 U). For U = 8 (G = 256):
-      // 9 shuffles + 9 HMNMX2 for all 8 groups, where one CREDUX pair per group needs 16
-      // CREDUX + 16 uniform-to-vector moves + 14 selects.
+      // (mn, inv) reach every lane through shared memory (GACT_Q_SMEMBC; else two shuffles
+      // from lane k << (5 - log2 U)). For U = 16 (G = 256): 16 shuffles + 16 HMNMX2 for all 16
+      // groups, where one CREDUX pair per group needs 32 CREDUX + 32 uniform-to-vector moves
+      // + 30 selects.
       constexpr int LU = U == 16 ? 4 : U == 8 ? 3 : U == 4 ? 2 : U == 2 ? 1 : 0;
       static_assert((1 << LU) == U, "U is a power of two <= 16");
       constexpr int SH = 5 - LU;
