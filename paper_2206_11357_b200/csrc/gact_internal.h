@@ -96,9 +96,19 @@ template <int MAXB>
 cudaError_t launch_dequantize(const DBatch<MAXB>& p, int dtype, int bits, cudaStream_t s);
 
 // Quantize tile: max(G, 256) elements for powers of two (a tile holds 256 / G groups below
-// 256), one group of G elements otherwise (the generic kernel: a warp per group).
+// 256); for other G above 256 one group (a warp per group); for other G below 256 (96, 160,
+// 192, 224) a super-tile of lcm(G, 256) elements = P = lcm / 256 warp passes holding lcm / G
+// whole groups.
 inline int64_t quantize_tile_elems(int32_t G) {
-  return group_log2(G) < 0 ? (int64_t)G : (G >= 256 ? (int64_t)G : 256);
+  if (group_log2(G) >= 0) return G >= 256 ? (int64_t)G : 256;
+  if (G > 256) return G;
+  int64_t a = G, b = 256;
+  while (b) {
+    const int64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return (int64_t)G / a * 256;
 }
 // Each tensor's quantize tile count is rounded up to this, so that a CTA unit (8 warps x up
 // to 8 consecutive tiles) never straddles two tensors of a batch.

@@ -158,6 +158,9 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 #ifndef GACT_BYTE2_MIX
 #define GACT_BYTE2_MIX 4  // G = 256: every 4th chunk packs by shift-add (0: every chunk byte-2)
 #endif
+#ifndef GACT_Q_ANYG_REG
+#define GACT_Q_ANYG_REG 1  // G not a power of two: the register-resident one-pass kernel
+#endif
 #ifndef GACT_Q_SMEMBC
 // 2-byte units: the groups' (mn, inv) reach the lanes through shared memory (one 8-byte
 // broadcast load per tile) instead of two shuffles per tile. A/B: single 2^28 bf16 G = 256
@@ -694,6 +697,188 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// The tensor's last group (short, or followed by the zero padding of the last word): the
+// two-pass generic path, out of line.
+template <int DT, int BITS, bool STATS>
+__device__ __noinline__ void group_generic(const QTensor T, int64_t g, int64_t G, float Lf, int lane) {
+  const int64_t e0 = g * G;
+  const int64_t e1 = e0 + G < T.n ? e0 + G : T.n;
+  float lmn = FLT_MAX, lmx = -FLT_MAX;
+  for (int64_t e = e0 + lane * kChunk; e < e1; e += 32 * kChunk) {
+    if (e + kChunk <= e1) {
+      Raw8<DT> raw;
+      load8<DT>(raw, T.x, e);
+      chunk_minmax_raw<DT>(raw, lmn, lmx);
+    } else {
+      for (int j = 0; j < kChunk; ++j) {
+        if (e + j < e1) {
+          const float x = load1<DT>(T.x, e + j);
+          lmn = fminf(lmn, x);
+          lmx = fmaxf(lmx, x);
+        }
+      }
+    }
+  }
+  const GroupParams gp = group_params(warp_min(lmn), warp_max(lmx), Lf);
+  if (lane == 0) {
+    T.group_min[g] = gp.mn;
+    T.group_scale[g] = gp.scale;
+  }
+  if constexpr (!STATS) {
+    for (int64_t e = e0 + lane * kChunk; e < e0 + G; e += 32 * kChunk) {
+      if (e + kChunk <= e1) {
+        Raw8<DT> raw;
+        load8<DT>(raw, T.x, e);
+        store_unit<BITS>(T.packed, e, quantize_chunk_raw<DT, BITS>(raw, gp.mn, gp.inv, chunk_rand(T, e)));
+      } else if ((e * BITS) / 32 < T.nwords) {
+        code_chunk_guarded<DT, BITS>(T, e, gp.mn, gp.inv);
+      }
+    }
+  }
+}
+
+// G a multiple of 32 that is not a power of two, one group per warp held in registers: lane l
+// owns the group's chunks l, l + 32, ... (at most NC of them, G <= 256 NC), loaded once; min /
+// max by CREDUX; codes from the same registers. Random bytes (R3): a lane's chunks sit 256
+// elements apart, so they pair up inside 512-element spans as the big kernel's do, except that
+// the first chunk may be the second half of its span (sh = 1): chunk i takes half (i + sh) & 1
+// of block slot (i + sh) >> 1, the slots being blk(e_first - 256 sh) + 32 j, computed with
+// their rounds 0-1 shared (philox4x32_10_xn). One pass over x (the two-pass kernel above is
+// kept for fp32 at G > 2048). A tensor's last group takes group_generic.
+template <int DT, int BITS, int MAXB, bool STATS, int NC>
+__global__ void __launch_bounds__(kThreads, (NC >= 16 || (DT == DT_F32 && NC >= 8)) ? 2 : 3)
+    quantize_anyg_reg_kernel(const __grid_constant__ QBatch<MAXB> P) {
+  constexpr int NB = NC / 2 + 1;  // block slots per lane
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
+  const int64_t G = P.group;
+  const int cpg = P.group / kChunk;  // chunks per group
+  const int64_t cunits = P.tiles_total / kWarps;
+  int cur = first_cursor(P, (int64_t)blockIdx.x * kWarps);
+  for (int64_t cu = blockIdx.x; cu < cunits; cu += gridDim.x) {
+    cur = advance_cursor(P, cur, cu * kWarps);
+    const QTensor& T = P.t[cur];
+    const int64_t g = cu * kWarps - P.tile_start[cur] + warp;
+    const int64_t e0 = g * G;
+    if (e0 >= T.n) continue;  // alignment padding of the tile space
+    if (e0 + G >= T.n) {      // the tensor's last group
+      group_generic<DT, BITS, STATS>(T, g, G, Lf, lane);
+      continue;
+    }
+    const int64_t e_lane = e0 + lane * kChunk;
+    Raw8<DT> raw[NC];
+#pragma unroll
+    for (int i = 0; i < NC; ++i)
+      if (lane + 32 * i < cpg) load8<DT>(raw[i], T.x, e_lane + i * kWarpTile);
+    uint4 r4[NB];
+    const int sh = (int)((e_lane >> 8) & 1);  // the lane's first chunk is the second half of its block
+    if constexpr (!STATS)
+      philox4x32_10_xn<NB>(rand_block(T, e_lane - 256 * sh), (uint32_t)T.seed, (uint32_t)(T.seed >> 32), r4);
+    float lmn = FLT_MAX, lmx = -FLT_MAX;  // neutral (lanes without chunks at G < 256)
+#pragma unroll
+    for (int i = 0; i < NC; ++i)
+      if (lane + 32 * i < cpg) chunk_minmax_raw<DT>(raw[i], lmn, lmx);
+    const GroupParams gp = group_params(warp_min(lmn), warp_max(lmx), Lf);
+    if (lane == 0) {
+      T.group_min[g] = gp.mn;
+      T.group_scale[g] = gp.scale;
+    }
+    if constexpr (!STATS) {
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+        if (lane + 32 * i < cpg) {
+          const uint4 q = sh ? r4[(i + 1) >> 1] : r4[i >> 1];  // half (i + sh) & 1 of slot (i + sh) >> 1
+          const uint2 rnd = ((i + sh) & 1) ? make_uint2(q.z, q.w) : make_uint2(q.x, q.y);
+          store_unit<BITS>(T.packed, e_lane + i * kWarpTile, quantize_chunk_raw<DT, BITS>(raw[i], gp.mn, gp.inv, rnd));
+        }
+      }
+    }
+  }
+}
+
+// G < 256 not a power of two (96, 160, 192, 224): a warp per super-tile of lcm(G, 256) = 256 P
+// elements (P = 3, 5, 3, 7 passes), which holds Q = 256 P / G whole groups of cpg = G / 8
+// chunks. Lane l loads its chunk of every pass (all 32 lanes busy, x read once); a group spans
+// whole aligned 4-lane blocks (cpg is a multiple of 4 and groups start at multiples of cpg), so
+// two butterfly steps give each block's (min, max); the 8 P block values go through shared
+// memory, lane q < Q folds its group's cpg / 4 blocks and computes the division, and each lane
+// reads its chunk's (mn, inv) back. Random bytes as in quantize_anyg_reg_kernel (the lane's
+// chunks 256 elements apart, first chunk possibly the second half of its block). A tensor's
+// last super-tile takes group_generic group by group.
+template <int DT, int BITS, int MAXB, bool STATS, int P>
+__global__ void __launch_bounds__(kThreads, 3)
+    quantize_anyg_small_kernel(const __grid_constant__ QBatch<MAXB> Pb) {
+  constexpr int NB = (P + 1) / 2 + 1;  // block slots per lane
+  __shared__ float2 blk[kWarps][8 * P];  // (min, max) of the super-tile's 4-lane blocks
+  __shared__ float2 gpar[kWarps][8];     // (mn, inv) of its groups
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const float Lf = STATS ? Pb.Lf : (float)((1 << BITS) - 1);
+  const int64_t G = Pb.group;
+  const int cpg = Pb.group / kChunk;           // chunks per group (12, 20, 24, 28)
+  const int bpg = cpg / 4;                     // 4-lane blocks per group
+  const int Q = 32 * P / cpg;                  // groups per super-tile (8 or 4)
+  const uint32_t rcp = (65536u + cpg - 1) / cpg;  // chunk c -> group (c rcp) >> 16, exact for c < 8 P 32
+  constexpr int64_t S = 256 * P;
+  const int64_t cunits = Pb.tiles_total / kWarps;
+  int cur = first_cursor(Pb, (int64_t)blockIdx.x * kWarps);
+  for (int64_t cu = blockIdx.x; cu < cunits; cu += gridDim.x) {
+    cur = advance_cursor(Pb, cur, cu * kWarps);
+    const QTensor& T = Pb.t[cur];
+    const int64_t e_tile = (cu * kWarps - Pb.tile_start[cur] + warp) * S;
+    if (e_tile >= T.n) continue;  // alignment padding of the tile space
+    const int64_t g0 = e_tile / G;
+    if (e_tile + S > T.n) {  // the tensor's last super-tile: group by group
+      for (int q = 0; q < Q; ++q)
+        if ((g0 + q) * G < T.n) group_generic<DT, BITS, STATS>(T, g0 + q, G, Lf, lane);
+      continue;
+    }
+    const int64_t e_lane = e_tile + lane * kChunk;
+    Raw8<DT> raw[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) load8<DT>(raw[p], T.x, e_lane + p * kWarpTile);
+    uint4 r4[NB];
+    const int sh = (int)((e_lane >> 8) & 1);
+    if constexpr (!STATS)
+      philox4x32_10_xn<NB>(rand_block(T, e_lane - 256 * sh), (uint32_t)T.seed, (uint32_t)(T.seed >> 32), r4);
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      float lmn = FLT_MAX, lmx = -FLT_MAX;
+      chunk_minmax_raw<DT>(raw[p], lmn, lmx);
+      lmn = fminf(lmn, __shfl_xor_sync(kFull, lmn, 1));
+      lmx = fmaxf(lmx, __shfl_xor_sync(kFull, lmx, 1));
+      lmn = fminf(lmn, __shfl_xor_sync(kFull, lmn, 2));
+      lmx = fmaxf(lmx, __shfl_xor_sync(kFull, lmx, 2));
+      if ((lane & 3) == 0) blk[warp][8 * p + (lane >> 2)] = make_float2(lmn, lmx);
+    }
+    __syncwarp();
+    if (lane < Q) {
+      float a = FLT_MAX, b = -FLT_MAX;
+      for (int k = 0; k < bpg; ++k) {
+        const float2 v = blk[warp][lane * bpg + k];
+        a = fminf(a, v.x);
+        b = fmaxf(b, v.y);
+      }
+      const GroupParams gp = group_params(a, b, Lf);
+      T.group_min[g0 + lane] = gp.mn;
+      T.group_scale[g0 + lane] = gp.scale;
+      gpar[warp][lane] = make_float2(gp.mn, gp.inv);
+    }
+    __syncwarp();
+    if constexpr (!STATS) {
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const float2 pq = gpar[warp][((uint32_t)(32 * p + lane) * rcp) >> 16];
+        const uint4 q = sh ? r4[(p + 1) >> 1] : r4[p >> 1];  // half (p + sh) & 1 of slot (p + sh) >> 1
+        const uint2 rnd = ((p + sh) & 1) ? make_uint2(q.z, q.w) : make_uint2(q.x, q.y);
+        store_unit<BITS>(T.packed, e_lane + p * kWarpTile, quantize_chunk_raw<DT, BITS>(raw[p], pq.x, pq.y, rnd));
+      }
+    }
+    __syncwarp();  // every lane has read blk / gpar before the next super-tile writes them
+  }
+}
+
 // ------------------------------------------------------------------------- launching
 template <typename K>
 int max_blocks_per_sm(K kernel) {
@@ -735,7 +920,23 @@ cudaError_t launch_units(const PB& p, int64_t tiles_per_unit, cudaStream_t s, in
 
 template <int DT, int BITS, int MAXB, bool STATS>
 cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
-  if (p.log2g < 0) return launch_units<quantize_anyg_kernel<DT, BITS, MAXB, STATS>>(p, kWarps, s, 8);
+  if (p.log2g < 0) {  // G not a power of two: a warp per group in registers (fp32: G <= 2048)
+    if (p.group < 256) {  // a warp per super-tile of lcm(G, 256) elements
+      const int P = (int)(quantize_tile_elems(p.group) / kWarpTile);
+      if (P == 3) return launch_units<quantize_anyg_small_kernel<DT, BITS, MAXB, STATS, 3>>(p, kWarps, s, 8);
+      if (P == 5) return launch_units<quantize_anyg_small_kernel<DT, BITS, MAXB, STATS, 5>>(p, kWarps, s, 8);
+      return launch_units<quantize_anyg_small_kernel<DT, BITS, MAXB, STATS, 7>>(p, kWarps, s, 8);
+    }
+#if GACT_Q_ANYG_REG
+    const int nc = (p.group + kWarpTile - 1) / kWarpTile;  // chunks per lane
+    if (nc <= 1) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 1>>(p, kWarps, s, 8);
+    if (nc <= 2) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 2>>(p, kWarps, s, 8);
+    if (nc <= 4) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 4>>(p, kWarps, s, 8);
+    if (nc <= 8) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 8>>(p, kWarps, s, 8);
+    if constexpr (DT != DT_F32) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 16>>(p, kWarps, s, 8);
+#endif
+    return launch_units<quantize_anyg_kernel<DT, BITS, MAXB, STATS>>(p, kWarps, s, 8);
+  }
   const int waves = DT == DT_F32 ? GACT_Q_WAVES_F32 : GACT_Q_WAVES;
   switch (p.log2g) {
     case 5:

@@ -189,7 +189,7 @@ def test_quantize_dequantize_parity(gact, orc, dtype, bits, G):
         check_dequantize(gact, orc, ct, ref, n, G, bits, ydt)
 
 
-GENERIC_GROUPS = [96, 160, 224, 288, 800, 1056, 2080, 4064]  # multiples of 32, not powers of two
+GENERIC_GROUPS = [96, 160, 192, 224, 288, 800, 1056, 2080, 4064]  # multiples of 32, not powers of two
 
 
 @pytest.mark.parametrize("dtype", DTYPES, ids=["f32", "bf16", "f16"])
@@ -210,10 +210,12 @@ def test_generic_group_sizes(gact, orc, dtype, bits, G):
         assert torch.equal(mn, ct.group_min) and torch.equal(sc, ct.group_scale)
 
 
-@pytest.mark.parametrize("G", [96, 1056])
+@pytest.mark.parametrize("G", [96, 192, 1056, 2080])
 def test_generic_group_sizes_batched(gact, orc, G):
     """Batched launches with a generic G: 40 ragged tensors of mixed dtype and bits, each
-    against the oracle (CTAs start at arbitrary tensors: binary-searched cursors)."""
+    against the oracle (CTAs start at arbitrary tensors: binary-searched cursors). G = 96 /
+    192: the super-tile kernel; 1056 / 2080: the register kernel (2-byte) and the two-pass
+    kernel (fp32 at 2080)."""
     rng = np.random.default_rng(G)
     xs, bits, seeds = [], [], []
     for i in range(40):
