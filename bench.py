@@ -328,7 +328,15 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         try:
-            e2e = run_e2e(args, gact, xs, D, B, c_local, seeds_base, G, s_in, dev, world)
+            # host buffers on the GPU's NUMA node: the e2e leg runs bound to its cores (at N = 1
+            # too; restored afterwards, so the CPU baseline below still sees every core)
+            saved = os.sched_getaffinity(0)
+            e2e_cores = pin_to_gpu_cpus(local)
+            try:
+                e2e = run_e2e(args, gact, xs, D, B, c_local, seeds_base, G, s_in, dev, world)
+            finally:
+                os.sched_setaffinity(0, saved)
+            e2e["cpu_affinity_cores"] = e2e_cores
         except (RuntimeError, MemoryError) as exc:  # e.g. pinned host memory exhausted
             e2e = {"value": None, "unit": "GB/s", "error": str(exc)[:200]}
 
