@@ -300,6 +300,7 @@ struct PackedUnit {
 #ifndef GACT_BYTE2_MAXB
 #define GACT_BYTE2_MAXB 4  // byte-2 codes up to this b (G = 256 kernel; b = 8 packs by byte permutes anyway)
 #endif
+static_assert(GACT_BYTE2_MAXB <= 4, "byte 2 of bits(v) holds q only while v < 256, i.e. b <= 4");
 #ifndef GACT_MAGIC_OFFSETS
 #define GACT_MAGIC_OFFSETS 1
 #endif
