@@ -21,7 +21,9 @@
 //    one recursive-halving butterfly (GACT_Q_XRED), each lane computes one group's division,
 //    and the groups' (mn, inv) reach the lanes through shared memory; otherwise FMNMX3
 //    in-thread, one CREDUX per group for min and max, divisions on U lanes, shuffles.
-//  * G in {32, 64, 128}: a tile holds 256/G groups of G/8 lanes; segmented shuffles.
+//  * G in {32, 64, 128}: a tile holds 256/G groups of G/8 lanes. 2-byte inputs: units of
+//    G / 8 tiles (16 at G = 32) reduced by one butterfly over the lane bits of a group's
+//    segment (quantize_smallx_kernel); fp32: segmented shuffles per tile.
 //  * G in {2048, 4096}, fp32: the group spans the CTA's registers (one HBM read).
 //  * G not a power of two: a warp per group, two passes (the second from L1 / L2).
 // A tensor's last tile may be partial (n % TE != 0): it takes the guarded generic path.
@@ -511,6 +513,9 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
 // ---------------------------------------------------------------------------------------
 // G in {32, 64, 128}: a 256-element tile holds 256/G groups of lpg = G/8 lanes each;
 // units of U tiles (U <= lpg: a group's U divisions run on U lanes of its segment).
+#ifndef GACT_QS_XRED
+#define GACT_QS_XRED 1  // 2-byte G = 32 / 64 / 128: quantize_smallx_kernel (butterfly over whole units)
+#endif
 #ifndef GACT_QS_UNIT
 #define GACT_QS_UNIT 8  // 2-byte inputs, G = 64 / 128: tiles per unit (G = 32 and fp32 keep 4)
 #endif
@@ -634,6 +639,97 @@ __global__ void __launch_bounds__(kThreads, GACT_QS_MINB)
         const float mn = __fadd_rn(mnk[k], 0.0f);
         store_unit_at<BITS>(out + (k * kWarpTile * BITS) / 8, quantize_chunk_raw<DT, BITS>(raw[k], mn, inv, rnd[k]));
       }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// G in {32, 64, 128}, 2-byte inputs: the G = 256 kernel's structure with a tile holding 256 / G
+// groups of lpg = G / 8 lanes. A warp unit is U = R lpg tiles (R = 2 at G = 32, else 1); every
+// lane folds its chunk of each tile into a packed (min, -max) pair, and a recursive-halving
+// butterfly over the lane bits inside a group's segment (xor lpg / 2, ..., 1) leaves lane l
+// with the groups of tiles R (l & (lpg - 1)) + r, r < R, in its own segment: U - R shuffles
+// per unit for all of the unit's groups (the segmented kernel above: log2(lpg) per tile).
+// Each lane computes R divisions; (mn, inv) reach the lanes through shared memory. A tensor's
+// last unit takes small_tile per tile. (G = 64 / 128 against the segmented kernel: bf16 2^28
+// b = 1-8 +9-10% / +13-19%.)
+template <int DT, int BITS, int MAXB, bool STATS, int LOG2G>
+__global__ void __launch_bounds__(kThreads, LOG2G >= 7 ? 2 : 3)
+    quantize_smallx_kernel(const __grid_constant__ QBatch<MAXB> P) {
+  static_assert(DT != DT_F32 && LOG2G >= 5 && LOG2G <= 7, "2-byte inputs, G = 32 / 64 / 128");
+  constexpr int lpg = 1 << (LOG2G - 3);  // lanes per group
+  constexpr int R = LOG2G == 5 ? 2 : 1;  // groups per lane per unit
+  constexpr int U = R * lpg;             // tiles per warp unit
+  constexpr int CU = kWarps * U;
+  constexpr int GPT = 32 / lpg;          // groups per tile
+  constexpr int LU = LOG2G - 3;          // butterfly levels
+  __shared__ float2 bc[kWarps][U][GPT];  // (mn, inv) of the unit's groups
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int seg = lane >> LU;            // the lane's group within a tile
+  const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
+  const int64_t cunits = P.tiles_total / CU;
+  int cur = first_cursor(P, (int64_t)blockIdx.x * CU);
+  for (int64_t cu = blockIdx.x; cu < cunits; cu += gridDim.x) {
+    cur = advance_cursor(P, cur, cu * CU);
+    const QTensor& T = P.t[cur];
+    const int64_t e_warp = (cu * CU - P.tile_start[cur] + (int64_t)warp * U) * kWarpTile;
+    const int64_t e_lane = e_warp + lane * kChunk;
+    if (e_warp + U * kWarpTile > T.n) {  // the tensor's last units: tile by tile, guarded
+      for (int k = 0; k < U; ++k) {
+        const int64_t t0 = e_warp + k * kWarpTile;
+        if (t0 >= T.n) break;  // warp-uniform: the rest of the unit is padding
+        const int64_t e = e_lane + k * kWarpTile;
+        Raw8<DT> raw;
+        const bool full = t0 + kWarpTile <= T.n;
+        if (full) load8<DT>(raw, T.x, e);
+        small_tile<DT, BITS, STATS>(T, e, full, raw, STATS ? make_uint2(0, 0) : chunk_rand(T, e), LOG2G, lpg, Lf, lane);
+      }
+      continue;
+    }
+    Raw8<DT> raw[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) load8<DT>(raw[k], T.x, e_lane + k * kWarpTile);
+    uint2 rnd[U];
+    if constexpr (!STATS) {
+      uint4 r4[U / 2];
+      philox4x32_10_xn<U / 2>(rand_block(T, e_lane), (uint32_t)T.seed, (uint32_t)(T.seed >> 32), r4);
+#pragma unroll
+      for (int k = 0; k < U; ++k) rnd[k] = (k & 1) ? make_uint2(r4[k >> 1].z, r4[k >> 1].w) : make_uint2(r4[k >> 1].x, r4[k >> 1].y);
+    }
+    uint32_t p[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) p[k] = chunk_minnegmax_packed<DT>(raw[k]);
+#pragma unroll
+    for (int lvl = 0; lvl < LU; ++lvl) {
+      const int mask = (lpg >> 1) >> lvl, half = U >> (lvl + 1);
+      const bool upper = lane & mask;
+#pragma unroll
+      for (int j = 0; j < half; ++j) {
+        const uint32_t send = upper ? p[j] : p[j + half], keep = upper ? p[j + half] : p[j];
+        p[j] = min2_packed<DT>(keep, __shfl_xor_sync(kFull, send, mask));
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float a, b;
+      unpack_minmax<DT>(p[r], a, b);
+      const GroupParams gp = group_params(a, b, Lf);
+      const int t = R * (lane & (lpg - 1)) + r;  // tile of the lane's r-th group
+      const int64_t g = (e_warp + t * kWarpTile) / (lpg * kChunk) + seg;
+      T.group_min[g] = gp.mn;
+      T.group_scale[g] = gp.scale;
+      if constexpr (!STATS) bc[warp][t][seg] = make_float2(gp.mn, gp.inv);
+    }
+    if constexpr (!STATS) {
+      __syncwarp();
+      unsigned char* out = reinterpret_cast<unsigned char*>(T.packed) + (e_lane * BITS) / 8;
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const float2 pk = bc[warp][k][seg];
+        store_unit_at<BITS>(out + (k * kWarpTile * BITS) / 8, quantize_chunk_raw<DT, BITS>(raw[k], pk.x, pk.y, rnd[k]));
+      }
+      __syncwarp();  // every lane has read bc[warp] before the next unit writes it
     }
   }
 }
@@ -940,10 +1036,19 @@ cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
   const int waves = DT == DT_F32 ? GACT_Q_WAVES_F32 : GACT_Q_WAVES;
   switch (p.log2g) {
     case 5:
+#if GACT_QS_XRED
+      if constexpr (DT != DT_F32) return launch_persistent<quantize_smallx_kernel<DT, BITS, MAXB, STATS, 5>>(p, 8, s, waves);
+#endif
       return launch_persistent<quantize_small_kernel<DT, BITS, MAXB, STATS, 5>>(p, small_unit<DT, 5>(), s, waves);
     case 6:
+#if GACT_QS_XRED
+      if constexpr (DT != DT_F32) return launch_persistent<quantize_smallx_kernel<DT, BITS, MAXB, STATS, 6>>(p, 8, s, waves);
+#endif
       return launch_persistent<quantize_small_kernel<DT, BITS, MAXB, STATS, 6>>(p, small_unit<DT, 6>(), s, waves);
     case 7:
+#if GACT_QS_XRED
+      if constexpr (DT != DT_F32) return launch_persistent<quantize_smallx_kernel<DT, BITS, MAXB, STATS, 7>>(p, 16, s, waves);
+#endif
       return launch_persistent<quantize_small_kernel<DT, BITS, MAXB, STATS, 7>>(p, small_unit<DT, 7>(), s, waves);
     case 8:
       return launch_persistent<quantize_big_kernel<DT, BITS, 1, MAXB, STATS>>(p, unit_tiles<DT, BITS, MAXB, 1>(), s, waves);
