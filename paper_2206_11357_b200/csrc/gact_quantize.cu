@@ -516,6 +516,9 @@ __global__ void __launch_bounds__(kThreads, GACT_Q_MINB)
 #ifndef GACT_QS_XRED
 #define GACT_QS_XRED 1  // 2-byte G = 32 / 64 / 128: quantize_smallx_kernel (butterfly over whole units)
 #endif
+#ifndef GACT_QSX_MIX
+#define GACT_QSX_MIX 4  // quantize_smallx_kernel: byte-2 codes for all but every 4th tile (A/B: b <= 2 +1%)
+#endif
 #ifndef GACT_QS_UNIT
 #define GACT_QS_UNIT 8  // 2-byte inputs, G = 64 / 128: tiles per unit (G = 32 and fp32 keep 4)
 #endif
@@ -727,7 +730,11 @@ __global__ void __launch_bounds__(kThreads, LOG2G >= 7 ? 2 : 3)
 #pragma unroll
       for (int k = 0; k < U; ++k) {
         const float2 pk = bc[warp][k][seg];
-        store_unit_at<BITS>(out + (k * kWarpTile * BITS) / 8, quantize_chunk_raw<DT, BITS>(raw[k], pk.x, pk.y, rnd[k]));
+        unsigned char* o = out + (k * kWarpTile * BITS) / 8;
+        if (GACT_QSX_MIX > 0 && k % (GACT_QSX_MIX > 0 ? GACT_QSX_MIX : 1) != GACT_QSX_MIX - 1)
+          store_unit_at<BITS>(o, quantize_chunk_raw<DT, BITS, true>(raw[k], pk.x, pk.y, rnd[k]));
+        else
+          store_unit_at<BITS>(o, quantize_chunk_raw<DT, BITS, false>(raw[k], pk.x, pk.y, rnd[k]));
       }
       __syncwarp();  // every lane has read bc[warp] before the next unit writes it
     }
