@@ -160,6 +160,12 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 #ifndef GACT_BYTE2_MIX
 #define GACT_BYTE2_MIX 4  // G = 256: every 4th chunk packs by shift-add (0: every chunk byte-2)
 #endif
+#ifndef GACT_ANYG_K3
+#define GACT_ANYG_K3 2  // G = 96 / 192, 2-byte: super-tiles per warp iteration (1 / 2 / 4 measured; 2 best, +9%)
+#endif
+#ifndef GACT_ANYG_K5
+#define GACT_ANYG_K5 1  // G = 160, 2-byte (2 measured 3% slower)
+#endif
 #ifndef GACT_Q_ANYG_REG
 #define GACT_Q_ANYG_REG 1  // G not a power of two: the register-resident one-pass kernel
 #endif
@@ -909,44 +915,46 @@ __global__ void __launch_bounds__(kThreads, (NC >= 16 || (DT == DT_F32 && NC >= 
 // reads its chunk's (mn, inv) back. Random bytes as in quantize_anyg_reg_kernel (the lane's
 // chunks 256 elements apart, first chunk possibly the second half of its block). A tensor's
 // last super-tile takes group_generic group by group.
-template <int DT, int BITS, int MAXB, bool STATS, int P>
+template <int DT, int BITS, int MAXB, bool STATS, int P, int K>
 __global__ void __launch_bounds__(kThreads, 3)
     quantize_anyg_small_kernel(const __grid_constant__ QBatch<MAXB> Pb) {
-  constexpr int NB = (P + 1) / 2 + 1;  // block slots per lane
-  __shared__ float2 blk[kWarps][8 * P];  // (min, max) of the super-tile's 4-lane blocks
-  __shared__ float2 gpar[kWarps][8];     // (mn, inv) of its groups
+  constexpr int PK = P * K;             // passes per warp iteration (K super-tiles)
+  constexpr int NB = (PK + 1) / 2 + 1;  // block slots per lane
+  __shared__ float2 blk[kWarps][8 * PK];  // (min, max) of the 4-lane blocks
+  __shared__ float2 gpar[kWarps][32];     // (mn, inv) of the groups
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const float Lf = STATS ? Pb.Lf : (float)((1 << BITS) - 1);
   const int64_t G = Pb.group;
   const int cpg = Pb.group / kChunk;           // chunks per group (12, 20, 24, 28)
   const int bpg = cpg / 4;                     // 4-lane blocks per group
-  const int Q = 32 * P / cpg;                  // groups per super-tile (8 or 4)
-  const uint32_t rcp = (65536u + cpg - 1) / cpg;  // chunk c -> group (c rcp) >> 16, exact for c < 8 P 32
-  constexpr int64_t S = 256 * P;
-  const int64_t cunits = Pb.tiles_total / kWarps;
-  int cur = first_cursor(Pb, (int64_t)blockIdx.x * kWarps);
+  const int Q = K * (32 * P / cpg);            // groups per warp iteration (<= 32)
+  const uint32_t rcp = (65536u + cpg - 1) / cpg;  // chunk c -> group (c rcp) >> 16, exact for c < 32 PK
+  constexpr int64_t S = 256 * P;               // one super-tile (the host's quantize tile)
+  constexpr int CU = kWarps * K;
+  const int64_t cunits = Pb.tiles_total / CU;
+  int cur = first_cursor(Pb, (int64_t)blockIdx.x * CU);
   for (int64_t cu = blockIdx.x; cu < cunits; cu += gridDim.x) {
-    cur = advance_cursor(Pb, cur, cu * kWarps);
+    cur = advance_cursor(Pb, cur, cu * CU);
     const QTensor& T = Pb.t[cur];
-    const int64_t e_tile = (cu * kWarps - Pb.tile_start[cur] + warp) * S;
+    const int64_t e_tile = (cu * CU - Pb.tile_start[cur] + (int64_t)warp * K) * S;
     if (e_tile >= T.n) continue;  // alignment padding of the tile space
     const int64_t g0 = e_tile / G;
-    if (e_tile + S > T.n) {  // the tensor's last super-tile: group by group
+    if (e_tile + K * S > T.n) {  // the tensor's last super-tiles: group by group
       for (int q = 0; q < Q; ++q)
         if ((g0 + q) * G < T.n) group_generic<DT, BITS, STATS>(T, g0 + q, G, Lf, lane);
       continue;
     }
     const int64_t e_lane = e_tile + lane * kChunk;
-    Raw8<DT> raw[P];
+    Raw8<DT> raw[PK];
 #pragma unroll
-    for (int p = 0; p < P; ++p) load8<DT>(raw[p], T.x, e_lane + p * kWarpTile);
+    for (int p = 0; p < PK; ++p) load8<DT>(raw[p], T.x, e_lane + p * kWarpTile);
     uint4 r4[NB];
     const int sh = (int)((e_lane >> 8) & 1);
     if constexpr (!STATS)
       philox4x32_10_xn<NB>(rand_block(T, e_lane - 256 * sh), (uint32_t)T.seed, (uint32_t)(T.seed >> 32), r4);
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
+    for (int p = 0; p < PK; ++p) {
       float lmn = FLT_MAX, lmx = -FLT_MAX;
       chunk_minmax_raw<DT>(raw[p], lmn, lmx);
       lmn = fminf(lmn, __shfl_xor_sync(kFull, lmn, 1));
@@ -971,7 +979,7 @@ __global__ void __launch_bounds__(kThreads, 3)
     __syncwarp();
     if constexpr (!STATS) {
 #pragma unroll
-      for (int p = 0; p < P; ++p) {
+      for (int p = 0; p < PK; ++p) {
         const float2 pq = gpar[warp][((uint32_t)(32 * p + lane) * rcp) >> 16];
         const uint4 q = sh ? r4[(p + 1) >> 1] : r4[p >> 1];  // half (p + sh) & 1 of slot (p + sh) >> 1
         const uint2 rnd = ((p + sh) & 1) ? make_uint2(q.z, q.w) : make_uint2(q.x, q.y);
@@ -1025,10 +1033,12 @@ template <int DT, int BITS, int MAXB, bool STATS>
 cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
   if (p.log2g < 0) {  // G not a power of two: a warp per group in registers (fp32: G <= 2048)
     if (p.group < 256) {  // a warp per super-tile of lcm(G, 256) elements
+      // K super-tiles per warp iteration (2-byte G = 96 / 192: 2, i.e. 6 passes; fp32: 1)
+      constexpr int K3 = DT == DT_F32 ? 1 : GACT_ANYG_K3, K5 = DT == DT_F32 ? 1 : GACT_ANYG_K5;
       const int P = (int)(quantize_tile_elems(p.group) / kWarpTile);
-      if (P == 3) return launch_units<quantize_anyg_small_kernel<DT, BITS, MAXB, STATS, 3>>(p, kWarps, s, 8);
-      if (P == 5) return launch_units<quantize_anyg_small_kernel<DT, BITS, MAXB, STATS, 5>>(p, kWarps, s, 8);
-      return launch_units<quantize_anyg_small_kernel<DT, BITS, MAXB, STATS, 7>>(p, kWarps, s, 8);
+      if (P == 3) return launch_units<quantize_anyg_small_kernel<DT, BITS, MAXB, STATS, 3, K3>>(p, kWarps * K3, s, 8);
+      if (P == 5) return launch_units<quantize_anyg_small_kernel<DT, BITS, MAXB, STATS, 5, K5>>(p, kWarps * K5, s, 8);
+      return launch_units<quantize_anyg_small_kernel<DT, BITS, MAXB, STATS, 7, 1>>(p, kWarps, s, 8);
     }
 #if GACT_Q_ANYG_REG
     const int nc = (p.group + kWarpTile - 1) / kWarpTile;  // chunks per lane
