@@ -956,11 +956,18 @@ __global__ void __launch_bounds__(kThreads, 3)
 #pragma unroll
     for (int p = 0; p < PK; ++p) {
       float lmn = FLT_MAX, lmx = -FLT_MAX;
-      chunk_minmax_raw<DT>(raw[p], lmn, lmx);
-      lmn = fminf(lmn, __shfl_xor_sync(kFull, lmn, 1));
-      lmx = fmaxf(lmx, __shfl_xor_sync(kFull, lmx, 1));
-      lmn = fminf(lmn, __shfl_xor_sync(kFull, lmn, 2));
-      lmx = fmaxf(lmx, __shfl_xor_sync(kFull, lmx, 2));
+      if constexpr (DT != DT_F32) {  // packed (min, -max): one shuffle + one HMNMX2 per step
+        uint32_t pm = chunk_minnegmax_packed<DT>(raw[p]);
+        pm = min2_packed<DT>(pm, __shfl_xor_sync(kFull, pm, 1));
+        pm = min2_packed<DT>(pm, __shfl_xor_sync(kFull, pm, 2));
+        unpack_minmax<DT>(pm, lmn, lmx);
+      } else {
+        chunk_minmax_raw<DT>(raw[p], lmn, lmx);
+        lmn = fminf(lmn, __shfl_xor_sync(kFull, lmn, 1));
+        lmx = fmaxf(lmx, __shfl_xor_sync(kFull, lmx, 1));
+        lmn = fminf(lmn, __shfl_xor_sync(kFull, lmn, 2));
+        lmx = fmaxf(lmx, __shfl_xor_sync(kFull, lmx, 2));
+      }
       if ((lane & 3) == 0) blk[warp][8 * p + (lane >> 2)] = make_float2(lmn, lmx);
     }
     __syncwarp();
@@ -983,7 +990,10 @@ __global__ void __launch_bounds__(kThreads, 3)
         const float2 pq = gpar[warp][((uint32_t)(32 * p + lane) * rcp) >> 16];
         const uint4 q = sh ? r4[(p + 1) >> 1] : r4[p >> 1];  // half (p + sh) & 1 of slot (p + sh) >> 1
         const uint2 rnd = ((p + sh) & 1) ? make_uint2(q.z, q.w) : make_uint2(q.x, q.y);
-        store_unit<BITS>(T.packed, e_lane + p * kWarpTile, quantize_chunk_raw<DT, BITS>(raw[p], pq.x, pq.y, rnd));
+        if (DT != DT_F32 && p % 4 != 3)  // byte-2 codes, one pass in four on shift-add (pipe balance)
+          store_unit<BITS>(T.packed, e_lane + p * kWarpTile, quantize_chunk_raw<DT, BITS, true>(raw[p], pq.x, pq.y, rnd));
+        else
+          store_unit<BITS>(T.packed, e_lane + p * kWarpTile, quantize_chunk_raw<DT, BITS, false>(raw[p], pq.x, pq.y, rnd));
       }
     }
     __syncwarp();  // every lane has read blk / gpar before the next super-tile writes them
