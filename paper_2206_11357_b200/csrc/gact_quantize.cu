@@ -166,6 +166,9 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 #ifndef GACT_ANYG_K5
 #define GACT_ANYG_K5 1  // G = 160, 2-byte (2 measured 3% slower)
 #endif
+#ifndef GACT_ANYG_MG2
+#define GACT_ANYG_MG2 1  // G > 256 not a power of two: two groups per warp iteration where they fit (G = 288 +57%, 800 +6-22%)
+#endif
 #ifndef GACT_Q_ANYG_REG
 #define GACT_Q_ANYG_REG 1  // G not a power of two: the register-resident one-pass kernel
 #endif
@@ -854,52 +857,81 @@ __device__ __noinline__ void group_generic(const QTensor T, int64_t g, int64_t G
 // of block slot (i + sh) >> 1, the slots being blk(e_first - 256 sh) + 32 j, computed with
 // their rounds 0-1 shared (philox4x32_10_xn). One pass over x (the two-pass kernel above is
 // kept for fp32 at G > 2048). A tensor's last group takes group_generic.
-template <int DT, int BITS, int MAXB, bool STATS, int NC>
+// MG = 2: a warp takes two consecutive groups as one span of 2 G elements (chunk j of the span
+// belongs to group j >= cpg; lanes stay busy across the groups' boundary); two CREDUX pairs,
+// the two divisions on lanes 0 / 1, (mn, inv) broadcast by shuffles.
+template <int DT, int BITS, int MAXB, bool STATS, int NC, int MG>
 __global__ void __launch_bounds__(kThreads, (NC >= 16 || (DT == DT_F32 && NC >= 8)) ? 2 : 3)
     quantize_anyg_reg_kernel(const __grid_constant__ QBatch<MAXB> P) {
+  static_assert(MG == 1 || MG == 2, "one or two groups per warp iteration");
   constexpr int NB = NC / 2 + 1;  // block slots per lane
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const float Lf = STATS ? P.Lf : (float)((1 << BITS) - 1);
   const int64_t G = P.group;
   const int cpg = P.group / kChunk;  // chunks per group
-  const int64_t cunits = P.tiles_total / kWarps;
-  int cur = first_cursor(P, (int64_t)blockIdx.x * kWarps);
+  constexpr int CU = kWarps * MG;
+  const int64_t cunits = P.tiles_total / CU;
+  int cur = first_cursor(P, (int64_t)blockIdx.x * CU);
   for (int64_t cu = blockIdx.x; cu < cunits; cu += gridDim.x) {
-    cur = advance_cursor(P, cur, cu * kWarps);
+    cur = advance_cursor(P, cur, cu * CU);
     const QTensor& T = P.t[cur];
-    const int64_t g = cu * kWarps - P.tile_start[cur] + warp;
+    const int64_t g = cu * CU - P.tile_start[cur] + (int64_t)warp * MG;
     const int64_t e0 = g * G;
     if (e0 >= T.n) continue;  // alignment padding of the tile space
-    if (e0 + G >= T.n) {      // the tensor's last group
-      group_generic<DT, BITS, STATS>(T, g, G, Lf, lane);
+    if (e0 + MG * G >= T.n) {  // the tensor's last group(s)
+      for (int q = 0; q < MG; ++q)
+        if ((g + q) * G < T.n) group_generic<DT, BITS, STATS>(T, g + q, G, Lf, lane);
       continue;
     }
+    const int span = MG * cpg;  // chunks of the warp's groups
     const int64_t e_lane = e0 + lane * kChunk;
     Raw8<DT> raw[NC];
 #pragma unroll
     for (int i = 0; i < NC; ++i)
-      if (lane + 32 * i < cpg) load8<DT>(raw[i], T.x, e_lane + i * kWarpTile);
+      if (lane + 32 * i < span) load8<DT>(raw[i], T.x, e_lane + i * kWarpTile);
     uint4 r4[NB];
     const int sh = (int)((e_lane >> 8) & 1);  // the lane's first chunk is the second half of its block
     if constexpr (!STATS)
       philox4x32_10_xn<NB>(rand_block(T, e_lane - 256 * sh), (uint32_t)T.seed, (uint32_t)(T.seed >> 32), r4);
-    float lmn = FLT_MAX, lmx = -FLT_MAX;  // neutral (lanes without chunks at G < 256)
+    float mn0 = FLT_MAX, mx0 = -FLT_MAX, mn1 = FLT_MAX, mx1 = -FLT_MAX;  // neutral
 #pragma unroll
-    for (int i = 0; i < NC; ++i)
-      if (lane + 32 * i < cpg) chunk_minmax_raw<DT>(raw[i], lmn, lmx);
-    const GroupParams gp = group_params(warp_min(lmn), warp_max(lmx), Lf);
-    if (lane == 0) {
-      T.group_min[g] = gp.mn;
-      T.group_scale[g] = gp.scale;
+    for (int i = 0; i < NC; ++i) {
+      const int j = lane + 32 * i;
+      if (j < span) {
+        if (MG == 1 || j < cpg) chunk_minmax_raw<DT>(raw[i], mn0, mx0);
+        else chunk_minmax_raw<DT>(raw[i], mn1, mx1);
+      }
+    }
+    GroupParams gp0, gp1;
+    if constexpr (MG == 1) {
+      gp0 = group_params(warp_min(mn0), warp_max(mx0), Lf);
+      if (lane == 0) {
+        T.group_min[g] = gp0.mn;
+        T.group_scale[g] = gp0.scale;
+      }
+    } else {
+      const float a0 = warp_min(mn0), b0 = warp_max(mx0), a1 = warp_min(mn1), b1 = warp_max(mx1);
+      const GroupParams gq = group_params(lane & 1 ? a1 : a0, lane & 1 ? b1 : b0, Lf);  // lane q: group q
+      if (lane < 2) {
+        T.group_min[g + lane] = gq.mn;
+        T.group_scale[g + lane] = gq.scale;
+      }
+      gp0.mn = __shfl_sync(kFull, gq.mn, 0);
+      gp0.inv = __shfl_sync(kFull, gq.inv, 0);
+      gp1.mn = __shfl_sync(kFull, gq.mn, 1);
+      gp1.inv = __shfl_sync(kFull, gq.inv, 1);
     }
     if constexpr (!STATS) {
 #pragma unroll
       for (int i = 0; i < NC; ++i) {
-        if (lane + 32 * i < cpg) {
+        const int j = lane + 32 * i;
+        if (j < span) {
           const uint4 q = sh ? r4[(i + 1) >> 1] : r4[i >> 1];  // half (i + sh) & 1 of slot (i + sh) >> 1
           const uint2 rnd = ((i + sh) & 1) ? make_uint2(q.z, q.w) : make_uint2(q.x, q.y);
-          store_unit<BITS>(T.packed, e_lane + i * kWarpTile, quantize_chunk_raw<DT, BITS>(raw[i], gp.mn, gp.inv, rnd));
+          const bool second = MG == 2 && j >= cpg;
+          store_unit<BITS>(T.packed, e_lane + i * kWarpTile,
+                           quantize_chunk_raw<DT, BITS>(raw[i], second ? gp1.mn : gp0.mn, second ? gp1.inv : gp0.inv, rnd));
         }
       }
     }
@@ -1051,12 +1083,15 @@ cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
       return launch_units<quantize_anyg_small_kernel<DT, BITS, MAXB, STATS, 7, 1>>(p, kWarps, s, 8);
     }
 #if GACT_Q_ANYG_REG
-    const int nc = (p.group + kWarpTile - 1) / kWarpTile;  // chunks per lane
-    if (nc <= 1) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 1>>(p, kWarps, s, 8);
-    if (nc <= 2) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 2>>(p, kWarps, s, 8);
-    if (nc <= 4) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 4>>(p, kWarps, s, 8);
-    if (nc <= 8) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 8>>(p, kWarps, s, 8);
-    if constexpr (DT != DT_F32) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 16>>(p, kWarps, s, 8);
+    // chunks per lane for one / two groups per warp iteration (two where they fit in 16 / 8)
+    const int nc1 = (p.group + kWarpTile - 1) / kWarpTile, nc2 = (2 * p.group + kWarpTile - 1) / kWarpTile;
+    constexpr int NCMAX = DT == DT_F32 ? 8 : 16;
+    if (GACT_ANYG_MG2 && nc2 <= 4) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 4, 2>>(p, kWarps * 2, s, 8);
+    if (GACT_ANYG_MG2 && nc2 <= 8) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 8, 2>>(p, kWarps * 2, s, 8);
+    if (GACT_ANYG_MG2 && nc2 <= NCMAX) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, NCMAX, 2>>(p, kWarps * 2, s, 8);
+    if (nc1 <= 4) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 4, 1>>(p, kWarps, s, 8);
+    if (nc1 <= 8) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 8, 1>>(p, kWarps, s, 8);
+    if constexpr (DT != DT_F32) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 16, 1>>(p, kWarps, s, 8);
 #endif
     return launch_units<quantize_anyg_kernel<DT, BITS, MAXB, STATS>>(p, kWarps, s, 8);
   }
