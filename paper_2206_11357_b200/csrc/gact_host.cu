@@ -124,7 +124,7 @@ cudaError_t enqueue_quantize(const QItem* items, int32_t count, int32_t G, cudaS
         if (it.t.n == 0 || it.dtype != dt || it.bits != bits) continue;
         p.tile_start[m] = tiles;
         p.t[m] = it.t;
-        tiles += quantize_tiles(it.t.n, G);
+        tiles += quantize_tiles(it.t.n, G, dt);
         ++m;
       }
       if (m == 0) break;
@@ -227,7 +227,7 @@ gact_status gact_group_stats(const void* x, int32_t dtype, int64_t n, int32_t gr
   p.Lf = (float)((1 << bits) - 1);
   p.t[0] = make_q(x, n, bits, 0, nullptr, group_min, group_scale);
   p.tile_start[0] = 0;
-  p.tiles_total = p.tile_start[1] = gact::quantize_tiles(n, group_size);
+  p.tiles_total = p.tile_start[1] = gact::quantize_tiles(n, group_size, dtype);
   return from_cuda(gact::launch_group_stats<1>(p, dtype, static_cast<cudaStream_t>(stream)));
 }
 
@@ -246,7 +246,7 @@ gact_status gact_quantize_pack(const void* x, int32_t dtype, int64_t n, int32_t 
   p.Lf = (float)((1 << bits) - 1);
   p.t[0] = make_q(x, n, bits, seed, packed, group_min, group_scale);
   p.tile_start[0] = 0;
-  p.tiles_total = p.tile_start[1] = gact::quantize_tiles(n, group_size);
+  p.tiles_total = p.tile_start[1] = gact::quantize_tiles(n, group_size, dtype);
   return from_cuda(gact::launch_quantize<1>(p, dtype, bits, static_cast<cudaStream_t>(stream)));
 }
 

@@ -87,7 +87,7 @@ inline uint64_t chunk_group_divisor(int32_t G) {
 }
 
 // Host-side launchers (gact_quantize.cu / gact_dequant.cu). Return cudaError_t of the launch.
-// `dtype` in {0,1,2}; `bits` in {1,2,4,8}. Tile sizes: quantize_tile_elems(G), dequant 256.
+// `dtype` in {0,1,2}; `bits` in {1,2,4,8}. Tile sizes: quantize_tile_elems(G, dtype), dequant 256.
 template <int MAXB>
 cudaError_t launch_quantize(const QBatch<MAXB>& p, int dtype, int bits, cudaStream_t s);
 template <int MAXB>
@@ -96,12 +96,12 @@ template <int MAXB>
 cudaError_t launch_dequantize(const DBatch<MAXB>& p, int dtype, int bits, cudaStream_t s);
 
 // Quantize tile: max(G, 256) elements for powers of two (a tile holds 256 / G groups below
-// 256); for other G above 256 one group (a warp per group); for other G below 256 (96, 160,
-// 192, 224) a super-tile of lcm(G, 256) elements = P = lcm / 256 warp passes holding lcm / G
-// whole groups.
-inline int64_t quantize_tile_elems(int32_t G) {
-  if (group_log2(G) >= 0) return G >= 256 ? (int64_t)G : 256;
-  if (G > 256) return G;
+// 256); for other G, a super-tile of lcm(G, 256) elements = P = lcm / 256 warp passes holding
+// lcm / G whole groups below 256 (and below 512 for 2-byte inputs), else one group (a warp per
+// group). `dtype`: GACT_F32 / GACT_BF16 / GACT_F16 (0 / 1 / 2).
+inline int64_t quantize_tile_elems(int32_t G, int32_t dtype) {
+  if (group_log2(G) >= 0) return G >= 256 ? G : 256;
+  if (G > 256 && (dtype == 0 || G > 512)) return G;
   int64_t a = G, b = 256;
   while (b) {
     const int64_t t = a % b;
@@ -116,8 +116,8 @@ inline int64_t quantize_tile_elems(int32_t G) {
 #define GACT_TILE_ALIGN 128
 #endif
 constexpr int64_t kTileAlign = GACT_TILE_ALIGN;
-inline int64_t quantize_tiles(int64_t n, int32_t G) {
-  const int64_t te = quantize_tile_elems(G);
+inline int64_t quantize_tiles(int64_t n, int32_t G, int32_t dtype) {
+  const int64_t te = quantize_tile_elems(G, dtype);
   const int64_t t = (n + te - 1) / te;
   return (t + kTileAlign - 1) / kTileAlign * kTileAlign;
 }

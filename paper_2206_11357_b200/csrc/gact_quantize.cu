@@ -938,9 +938,9 @@ __global__ void __launch_bounds__(kThreads, (NC >= 16 || (DT == DT_F32 && NC >= 
   }
 }
 
-// G < 256 not a power of two (96, 160, 192, 224): a warp per super-tile of lcm(G, 256) = 256 P
-// elements (P = 3, 5, 3, 7 passes), which holds Q = 256 P / G whole groups of cpg = G / 8
-// chunks. Lane l loads its chunk of every pass (all 32 lanes busy, x read once); a group spans
+// G < 256 not a power of two (96, 160, 192, 224; for 2-byte inputs also 288 ... 480): a warp
+// per super-tile of lcm(G, 256) = 256 P elements (P = 3 ... 15 passes), which holds Q = 256 P / G
+// whole groups of cpg = G / 8 chunks. Lane l loads its chunk of every pass (all 32 lanes busy, x read once); a group spans
 // whole aligned 4-lane blocks (cpg is a multiple of 4 and groups start at multiples of cpg), so
 // two butterfly steps give each block's (min, max); the 8 P block values go through shared
 // memory, lane q < Q folds its group's cpg / 4 blocks and computes the division, and each lane
@@ -948,7 +948,7 @@ __global__ void __launch_bounds__(kThreads, (NC >= 16 || (DT == DT_F32 && NC >= 
 // chunks 256 elements apart, first chunk possibly the second half of its block). A tensor's
 // last super-tile takes group_generic group by group.
 template <int DT, int BITS, int MAXB, bool STATS, int P, int K>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, P * K >= 9 ? 2 : 3)
     quantize_anyg_small_kernel(const __grid_constant__ QBatch<MAXB> Pb) {
   constexpr int PK = P * K;             // passes per warp iteration (K super-tiles)
   constexpr int NB = (PK + 1) / 2 + 1;  // block slots per lane
@@ -1074,13 +1074,19 @@ cudaError_t launch_units(const PB& p, int64_t tiles_per_unit, cudaStream_t s, in
 template <int DT, int BITS, int MAXB, bool STATS>
 cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
   if (p.log2g < 0) {  // G not a power of two: a warp per group in registers (fp32: G <= 2048)
-    if (p.group < 256) {  // a warp per super-tile of lcm(G, 256) elements
+    const int P = (int)(quantize_tile_elems(p.group, DT) / kWarpTile);
+    if (p.group < 256 || (DT != DT_F32 && p.group < 512)) {  // a warp per super-tile of lcm(G, 256)
       // K super-tiles per warp iteration (2-byte G = 96 / 192: 2, i.e. 6 passes; fp32: 1)
       constexpr int K3 = DT == DT_F32 ? 1 : GACT_ANYG_K3, K5 = DT == DT_F32 ? 1 : GACT_ANYG_K5;
-      const int P = (int)(quantize_tile_elems(p.group) / kWarpTile);
       if (P == 3) return launch_units<quantize_anyg_small_kernel<DT, BITS, MAXB, STATS, 3, K3>>(p, kWarps * K3, s, 8);
       if (P == 5) return launch_units<quantize_anyg_small_kernel<DT, BITS, MAXB, STATS, 5, K5>>(p, kWarps * K5, s, 8);
-      return launch_units<quantize_anyg_small_kernel<DT, BITS, MAXB, STATS, 7, 1>>(p, kWarps, s, 8);
+      if (P == 7) return launch_units<quantize_anyg_small_kernel<DT, BITS, MAXB, STATS, 7, 1>>(p, kWarps, s, 8);
+      if constexpr (DT != DT_F32) {  // 2-byte, 256 < G < 512: P = 9, 11, 13, 15
+        if (P == 9) return launch_units<quantize_anyg_small_kernel<DT, BITS, MAXB, STATS, 9, 1>>(p, kWarps, s, 8);
+        if (P == 11) return launch_units<quantize_anyg_small_kernel<DT, BITS, MAXB, STATS, 11, 1>>(p, kWarps, s, 8);
+        if (P == 13) return launch_units<quantize_anyg_small_kernel<DT, BITS, MAXB, STATS, 13, 1>>(p, kWarps, s, 8);
+        return launch_units<quantize_anyg_small_kernel<DT, BITS, MAXB, STATS, 15, 1>>(p, kWarps, s, 8);
+      }
     }
 #if GACT_Q_ANYG_REG
     // chunks per lane for one / two groups per warp iteration (two where they fit in 16 / 8)

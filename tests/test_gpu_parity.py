@@ -189,7 +189,7 @@ def test_quantize_dequantize_parity(gact, orc, dtype, bits, G):
         check_dequantize(gact, orc, ct, ref, n, G, bits, ydt)
 
 
-GENERIC_GROUPS = [96, 160, 192, 224, 288, 800, 1056, 2080, 4064]  # multiples of 32, not powers of two
+GENERIC_GROUPS = [96, 160, 192, 224, 288, 320, 384, 480, 800, 1056, 2080, 4064]  # multiples of 32, not powers of two
 
 
 @pytest.mark.parametrize("dtype", DTYPES, ids=["f32", "bf16", "f16"])
@@ -210,7 +210,7 @@ def test_generic_group_sizes(gact, orc, dtype, bits, G):
         assert torch.equal(mn, ct.group_min) and torch.equal(sc, ct.group_scale)
 
 
-@pytest.mark.parametrize("G", [96, 192, 1056, 2080])
+@pytest.mark.parametrize("G", [96, 192, 352, 1056, 2080])
 def test_generic_group_sizes_batched(gact, orc, G):
     """Batched launches with a generic G: 40 ragged tensors of mixed dtype and bits, each
     against the oracle (CTAs start at arbitrary tensors: binary-searched cursors). G = 96 /
