@@ -861,7 +861,7 @@ __device__ __noinline__ void group_generic(const QTensor T, int64_t g, int64_t G
 // belongs to group j >= cpg; lanes stay busy across the groups' boundary); two CREDUX pairs,
 // the two divisions on lanes 0 / 1, (mn, inv) broadcast by shuffles.
 template <int DT, int BITS, int MAXB, bool STATS, int NC, int MG>
-__global__ void __launch_bounds__(kThreads, (NC >= 16 || (DT == DT_F32 && NC >= 8)) ? 2 : 3)
+__global__ void __launch_bounds__(kThreads, (NC >= 12 || (DT == DT_F32 && NC >= 8)) ? 2 : 3)
     quantize_anyg_reg_kernel(const __grid_constant__ QBatch<MAXB> P) {
   static_assert(MG == 1 || MG == 2, "one or two groups per warp iteration");
   constexpr int NB = NC / 2 + 1;  // block slots per lane
@@ -1094,6 +1094,8 @@ cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
     constexpr int NCMAX = DT == DT_F32 ? 8 : 16;
     if (GACT_ANYG_MG2 && nc2 <= 4) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 4, 2>>(p, kWarps * 2, s, 8);
     if (GACT_ANYG_MG2 && nc2 <= 8) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 8, 2>>(p, kWarps * 2, s, 8);
+    if constexpr (DT != DT_F32)
+      if (GACT_ANYG_MG2 && nc2 <= 12) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 12, 2>>(p, kWarps * 2, s, 8);
     if (GACT_ANYG_MG2 && nc2 <= NCMAX) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, NCMAX, 2>>(p, kWarps * 2, s, 8);
     if (nc1 <= 4) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 4, 1>>(p, kWarps, s, 8);
     if (nc1 <= 8) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 8, 1>>(p, kWarps, s, 8);
