@@ -1099,6 +1099,8 @@ cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
     if (GACT_ANYG_MG2 && nc2 <= NCMAX) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, NCMAX, 2>>(p, kWarps * 2, s, 8);
     if (nc1 <= 4) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 4, 1>>(p, kWarps, s, 8);
     if (nc1 <= 8) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 8, 1>>(p, kWarps, s, 8);
+    if constexpr (DT != DT_F32)
+      if (nc1 <= 12) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 12, 1>>(p, kWarps, s, 8);
     if constexpr (DT != DT_F32) return launch_units<quantize_anyg_reg_kernel<DT, BITS, MAXB, STATS, 16, 1>>(p, kWarps, s, 8);
 #endif
     return launch_units<quantize_anyg_kernel<DT, BITS, MAXB, STATS>>(p, kWarps, s, 8);
