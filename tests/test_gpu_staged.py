@@ -139,7 +139,7 @@ def test_staged_validation(gact):
                                        ws.data_ptr(), ws.numel(), s) == 0
 
 
-@pytest.mark.parametrize("G", [96, 1056, 4064])
+@pytest.mark.parametrize("G", [96, 288, 1056, 2080, 4064])
 @pytest.mark.parametrize("ws_bytes", [3 * (4 << 20), 3 * (64 << 20)])
 def test_staged_generic_group_sizes(gact, orc, G, ws_bytes):
     """Group sizes that are not powers of two stage in pieces of lcm(G, 4096) elements (a
