@@ -161,13 +161,16 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 #define GACT_BYTE2_MIX 4  // G = 256: every 4th chunk packs by shift-add (0: every chunk byte-2)
 #endif
 #ifndef GACT_ANYG_K3
-#define GACT_ANYG_K3 2  // G = 96 / 192, 2-byte: super-tiles per warp iteration (1 / 2 / 4 measured; 2 best, +9%)
+#define GACT_ANYG_K3 4  // G = 96 / 192, 2-byte: super-tiles per warp iteration (at 2 CTAs per SM; 2 / 4: +9% / +17% over 1)
 #endif
 #ifndef GACT_ANYG_K5
 #define GACT_ANYG_K5 1  // G = 160, 2-byte (2 measured 3% slower)
 #endif
 #ifndef GACT_ANYG_MG2
 #define GACT_ANYG_MG2 1  // G > 256 not a power of two: two groups per warp iteration where they fit (G = 288 +57%, 800 +6-22%)
+#endif
+#ifndef GACT_ANYG_SMALL_PK2
+#define GACT_ANYG_SMALL_PK2 6  // super-tile kernel: 2 CTAs per SM (128 registers) from this many passes (G = 224: +9%)
 #endif
 #ifndef GACT_Q_ANYG_REG
 #define GACT_Q_ANYG_REG 1  // G not a power of two: the register-resident one-pass kernel
@@ -948,7 +951,7 @@ __global__ void __launch_bounds__(kThreads, (NC >= 12 || (DT == DT_F32 && NC >= 
 // chunks 256 elements apart, first chunk possibly the second half of its block). A tensor's
 // last super-tile takes group_generic group by group.
 template <int DT, int BITS, int MAXB, bool STATS, int P, int K>
-__global__ void __launch_bounds__(kThreads, P * K >= 9 ? 2 : 3)
+__global__ void __launch_bounds__(kThreads, P * K >= GACT_ANYG_SMALL_PK2 ? 2 : 3)
     quantize_anyg_small_kernel(const __grid_constant__ QBatch<MAXB> Pb) {
   constexpr int PK = P * K;             // passes per warp iteration (K super-tiles)
   constexpr int NB = (PK + 1) / 2 + 1;  // block slots per lane
@@ -1076,7 +1079,7 @@ cudaError_t launch_q(const QBatch<MAXB>& p, cudaStream_t s) {
   if (p.log2g < 0) {  // G not a power of two: a warp per group in registers (fp32: G <= 2048)
     const int P = (int)(quantize_tile_elems(p.group, DT) / kWarpTile);
     if (p.group < 256 || (DT != DT_F32 && p.group < 512)) {  // a warp per super-tile of lcm(G, 256)
-      // K super-tiles per warp iteration (2-byte G = 96 / 192: 2, i.e. 6 passes; fp32: 1)
+      // K super-tiles per warp iteration (2-byte G = 96 / 192: 4, i.e. 12 passes; fp32: 1)
       constexpr int K3 = DT == DT_F32 ? 1 : GACT_ANYG_K3, K5 = DT == DT_F32 ? 1 : GACT_ANYG_K5;
       if (P == 3) return launch_units<quantize_anyg_small_kernel<DT, BITS, MAXB, STATS, 3, K3>>(p, kWarps * K3, s, 8);
       if (P == 5) return launch_units<quantize_anyg_small_kernel<DT, BITS, MAXB, STATS, 5, K5>>(p, kWarps * K5, s, 8);
