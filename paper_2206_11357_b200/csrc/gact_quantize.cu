@@ -164,7 +164,7 @@ __device__ __noinline__ void tile_generic(const QTensor T, int64_t e0, int log2g
 #define GACT_ANYG_K3 4  // G = 96 / 192, 2-byte: super-tiles per warp iteration (at 2 CTAs per SM; 2 / 4: +9% / +17% over 1)
 #endif
 #ifndef GACT_ANYG_K5
-#define GACT_ANYG_K5 1  // G = 160, 2-byte (2 measured 3% slower)
+#define GACT_ANYG_K5 2  // G = 160 / 320, 2-byte (at 2 CTAs per SM: +22% over 1)
 #endif
 #ifndef GACT_ANYG_MG2
 #define GACT_ANYG_MG2 1  // G > 256 not a power of two: two groups per warp iteration where they fit (G = 288 +57%, 800 +6-22%)
